@@ -1,0 +1,145 @@
+/* lp2d_b200.h — C ABI of the B200-native batch 2D-LP solver.
+ *
+ * Drop-in boundary for the reference's batch-solve path:
+ *
+ *   lp2d::batch_result lp2d::solve_batch(const batch&, const block_config&,
+ *                                        const tolerance&)
+ *     /root/reference/proj/include/lp2d/batch.hpp:303-371
+ *
+ * The reference is header-only C++ with no ABI (proj/README.md:15); this
+ * header is what a reference-side binding calls. Plain
+ * pointers and sizes only: no exceptions, no C++ or torch types cross it.
+ *
+ * Semantics per LP (serial.hpp:159-188): maximise c.x subject to the four box
+ * constraints x<=M, -x<=M, y<=M, -y<=M (positions 0..3, never permuted) and the
+ * user constraints a.x <= b inserted in the order perm[0..m-1]. Results are
+ * bit-identical to the reference's serial solver computing in the same scalar
+ * type (fp64: the reference itself; fp32: oracle/ restatement in float).
+ */
+#ifndef LP2D_B200_H
+#define LP2D_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes (0 = ok) ---------------------------------------------- */
+enum {
+  LP2D_OK = 0,
+  LP2D_ERR_EMPTY_BATCH = -1,    /* batch.hpp:306   "empty batch"            */
+  LP2D_ERR_PERM_COUNT = -2,     /* batch.hpp:307-310 one permutation per LP */
+  LP2D_ERR_PERM_LENGTH = -3,    /* batch.hpp:311-316 length mismatch        */
+  LP2D_ERR_BLOCK_WIDTH = -4,    /* batch.hpp:317-319 zero block width       */
+  LP2D_ERR_LAYOUT = -5,         /* offsets not 8-aligned / segment too short */
+  LP2D_ERR_BAD_PERM = -6,       /* a perm entry >= m (reported per LP too)  */
+  LP2D_ERR_ARG = -7,            /* null pointer / bad enum                  */
+  LP2D_ERR_UNSUPPORTED = -8,    /* size class not built                     */
+  LP2D_ERR_CUDA = -9,           /* CUDA runtime error (see last_error)      */
+};
+
+/* ---- per-LP status (the builder's extension of serial.hpp:34-43) -------- */
+enum {
+  LP2D_OPTIMAL = 0,     /* feasible, both defining constraints are user ones */
+  LP2D_INFEASIBLE = 1,  /* solution::infeasible()                            */
+  LP2D_UNBOUNDED = 2,   /* feasible, optimum held by a box edge (k < 4)      */
+  LP2D_INVALID = 255,   /* malformed input for this LP (perm out of range)   */
+};
+/* pair entries: original constraint index, box position k -> -(k+1),
+ * LP2D_PAIR_NONE when no constraint owns the endpoint. */
+#define LP2D_PAIR_NONE ((int32_t)0x80000000)
+
+enum { LP2D_MEM_HOST = 0, LP2D_MEM_DEVICE = 1 };
+enum { LP2D_SCHED_NAIVE = 0, LP2D_SCHED_BALANCED = 1 };
+enum { LP2D_PERM_U16 = 16, LP2D_PERM_U32 = 32 };
+
+/* Packed structure-of-arrays batch (replaces the AoS std::vector<problem> of
+ * serial.hpp:28-32 + batch.hpp:45-48).
+ *   LP j owns elements [offset[j], offset[j] + m[j]) of ax, ay, b and perm.
+ *   offset[j] must be a multiple of 8 and offset[j+1] - offset[j] >=
+ *   round_up(m[j], 8) (16-byte bulk-copy granularity); lp2dgpu_pack_offsets()
+ *   computes such offsets.
+ *   perm[offset[j] + i] is the original index (0..m[j]-1) of the constraint
+ *   inserted i-th (serial.hpp:126-146 permutation::order).
+ *   c[2j], c[2j+1] is the objective, bound_m[j] the box half-width M.
+ * Scalars are float for lp2dgpu_solve_f32 and double for lp2dgpu_solve_f64.
+ * mem says whether every array is host or device memory. In device mode
+ * max_m must be given (host scalar, max over m[j]); in host mode it is
+ * computed when 0. */
+typedef struct lp2d_batch_soa {
+  int64_t n;
+  const int32_t* m;
+  const int64_t* offset; /* [n+1] */
+  const void* ax;
+  const void* ay;
+  const void* b;
+  const void* perm;
+  int32_t perm_bits; /* LP2D_PERM_U16 (needs m <= 65536) or LP2D_PERM_U32 */
+  int32_t mem;       /* LP2D_MEM_HOST / LP2D_MEM_DEVICE */
+  const void* c;     /* [2n] */
+  const void* bound_m; /* [n] */
+  int64_t max_m;
+} lp2d_batch_soa;
+
+/* block_config (batch.hpp:50-58) + tolerance (core.hpp:59-68). */
+typedef struct lp2d_opts {
+  int32_t scheduler;   /* LP2D_SCHED_BALANCED (warp-cooperative work units,
+                          default) or LP2D_SCHED_NAIVE (thread per LP) */
+  int32_t block_width; /* must be > 0 (validated like batch.hpp:317); the GPU
+                          schedule is fixed by the kernel, see DESIGN.md */
+  int32_t n_gpus;      /* host mode: shard over this many visible devices
+                          (0 = all); replaces block_config::workers */
+  int32_t device;      /* device mode: device ordinal of the pointers */
+  void* stream;        /* device mode: cudaStream_t (NULL = legacy stream) */
+  double eps_parallel; /* core.hpp:60 (1e-12) */
+  double eps_feas;     /* core.hpp:61 (1e-9)  */
+} lp2d_opts;
+
+/* Outputs, n entries each (host or device per batch->mem). Optional members
+ * may be NULL. x/y/value are float for f32 and double for f64. */
+typedef struct lp2d_out {
+  uint8_t* status;
+  void* x;
+  void* y;
+  void* value;
+  int32_t* pair;              /* [2n], optional */
+  uint32_t* violation_events; /* optional, serial.hpp:148-151 */
+  uint64_t* work_units;       /* optional */
+} lp2d_out;
+
+void lp2dgpu_default_opts(lp2d_opts* opts);
+
+/* Solve a batch. Host mode: copies in, solves (sharded over n_gpus devices,
+ * one host thread per device) and copies out before returning. Device mode:
+ * enqueues on opts->stream and returns without synchronising. */
+int lp2dgpu_solve_f32(const lp2d_batch_soa* batch, const lp2d_opts* opts,
+                      lp2d_out* out);
+int lp2dgpu_solve_f64(const lp2d_batch_soa* batch, const lp2d_opts* opts,
+                      lp2d_out* out);
+
+/* Offsets for a batch of sizes m[0..n-1] satisfying the layout contract;
+ * writes offset[0..n] and returns the total element count. */
+int64_t lp2dgpu_pack_offsets(int64_t n, const int32_t* m, int64_t* offset);
+
+/* Device-side permutation generation (serial.hpp:138-146 shuffle with
+ * rng.hpp:64-68 seeds): perm for LP j is shuffle(m[j], seeds[j]). Device
+ * pointers, enqueued on stream. perm_bits as in lp2d_batch_soa. */
+int lp2dgpu_shuffle_device(int64_t n, const int32_t* m, const int64_t* offset,
+                           const uint64_t* seeds, void* perm, int32_t perm_bits,
+                           int32_t device, void* stream);
+
+/* Number of visible CUDA devices (0 when none). */
+int lp2dgpu_device_count(void);
+
+/* Thread-local message for the last non-zero return code. */
+const char* lp2dgpu_last_error(void);
+
+/* Library build identification string. */
+const char* lp2dgpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LP2D_B200_H */

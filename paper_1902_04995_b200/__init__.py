@@ -1,0 +1,13 @@
+"""B200-native batch 2D linear programming (Seidel / RGB, arXiv 1902.04995).
+
+Drop-in for the reference's lp2d::solve_batch path; see DESIGN.md.
+"""
+from . import lp2d  # noqa: F401
+from .lp2d import (  # noqa: F401
+    Batch, BatchResult, BlockConfig, DeviceBatch, GenKind, PackedBatch, PackedResult,
+    Permutation, Problem, SchedulerKind, Solution, Tolerance, derive_seed, gen, gen_mixed,
+    identity_permutation, lane_imbalance, replicate, shuffle, solve_batch, solve_device,
+    solve_packed,
+)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

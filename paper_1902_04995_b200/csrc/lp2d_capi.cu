@@ -1,0 +1,435 @@
+// lp2d_capi.cu — C ABI (include/lp2d_b200.h) over the sm_100a kernels.
+//
+// Replaces lp2d::solve_batch (/root/reference/proj/include/lp2d/batch.hpp:
+// 303-371): same validation and error cases (:305-320, returned as codes, not
+// exceptions), the reference's jthread block pool (:335-351) replaced by
+// LP-index sharding over GPUs (one host thread per device) and, inside a GPU,
+// by warps claiming LPs from an atomic ticket.
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/lp2d_b200.h"
+#include "lp2d_kernels.cuh"
+
+using namespace lp2d_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                     \
+  do {                                                                     \
+    cudaError_t e_ = (expr);                                               \
+    if (e_ != cudaSuccess) {                                               \
+      return fail(LP2D_ERR_CUDA, std::string(#expr) + ": " +               \
+                                     cudaGetErrorString(e_));              \
+    }                                                                      \
+  } while (0)
+
+constexpr int kCounterSlots = 4096;
+
+// Per-device state: ticket counters (self-resetting, round-robin slots) and a
+// grow-only scratch arena for host-mode calls.
+struct DeviceState {
+  std::mutex mu;
+  bool init = false;
+  int sm_count = 0;
+  uint32_t* counters = nullptr;
+  std::atomic<uint32_t> next_slot{0};
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  cudaStream_t stream = nullptr;
+};
+
+DeviceState g_dev[64];
+
+// Restores the caller's current device (torch and others rely on it).
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() { cudaGetDevice(&prev); }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int ensure_device(int dev) {
+  DeviceState& d = g_dev[dev];
+  if (d.init) return 0;
+  CUDA_TRY(cudaSetDevice(dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_TRY(cudaMalloc(&d.counters, sizeof(uint32_t) * 2 * kCounterSlots));
+  CUDA_TRY(cudaMemset(d.counters, 0, sizeof(uint32_t) * 2 * kCounterSlots));
+  CUDA_TRY(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaDeviceSynchronize());
+  d.init = true;
+  return 0;
+}
+
+uint32_t* take_counter(int dev) {
+  DeviceState& d = g_dev[dev];
+  const uint32_t s = d.next_slot.fetch_add(1) % kCounterSlots;
+  return d.counters + 2 * s;
+}
+
+int nslot_for(int64_t max_m) {
+  if (max_m <= 32) return 1;
+  if (max_m <= 64) return 2;
+  if (max_m <= 128) return 4;
+  if (max_m <= 256) return 8;
+  if (max_m <= 512) return 16;
+  if (max_m <= 1024) return 32;
+  return -1;
+}
+
+template <typename T>
+constexpr int max_nslot() {
+  return sizeof(T) == 4 ? 32 : 16;  // fp64 keeps m <= 512 in registers
+}
+
+// Eps_par rounded up by 2^-10 (relative), in T: the parallel-filter factor.
+template <typename T>
+double eps_hi_of(double eps_par) {
+  const T e = (T)eps_par;
+  T hi = (T)((double)e * (1.0 + 1.0 / 1024.0));
+  if ((double)hi < (double)e * (1.0 + 1.0 / 1024.0)) hi = std::nextafter(hi, (T)INFINITY);
+  return (double)hi;
+}
+
+template <typename T, typename P, int NSLOT>
+int launch_warp_kernel(KParams kp, int dev, cudaStream_t stream) {
+  using L = WarpLayout<T, P, NSLOT>;
+  auto kern = k_solve_warp<T, P, NSLOT>;
+  static int blocks_per_sm[64] = {0};
+  if (!blocks_per_sm[dev]) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L::kSmem));
+    int b = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kWarpsPerCta * 32,
+                                                           L::kSmem));
+    if (b < 1) return fail(LP2D_ERR_CUDA, "warp kernel does not fit on an SM");
+    blocks_per_sm[dev] = b;
+  }
+  const int64_t want = (kp.n_list + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int64_t maxb = (int64_t)blocks_per_sm[dev] * g_dev[dev].sm_count;
+  const int grid = (int)std::max<int64_t>(1, std::min(want, maxb));
+  kp.total_warps = grid * kWarpsPerCta;
+  kp.counter = take_counter(dev);
+  kern<<<grid, kWarpsPerCta * 32, L::kSmem, stream>>>(kp);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <typename T, typename P>
+int launch_by_slots(const KParams& kp, int nslot, int dev, cudaStream_t s) {
+  switch (nslot) {
+    case 1: return launch_warp_kernel<T, P, 1>(kp, dev, s);
+    case 2: return launch_warp_kernel<T, P, 2>(kp, dev, s);
+    case 4: return launch_warp_kernel<T, P, 4>(kp, dev, s);
+    case 8: return launch_warp_kernel<T, P, 8>(kp, dev, s);
+    case 16: return launch_warp_kernel<T, P, 16>(kp, dev, s);
+    case 32:
+      if constexpr (max_nslot<T>() >= 32) return launch_warp_kernel<T, P, 32>(kp, dev, s);
+      break;
+  }
+  return fail(LP2D_ERR_UNSUPPORTED, "constraint count above the register-resident size classes");
+}
+
+template <typename T>
+int launch_solve(const KParams& kp, int64_t max_m, int perm_bits, int sched, int dev,
+                 cudaStream_t s) {
+  if (kp.n_list == 0) return 0;
+  if (sched == LP2D_SCHED_NAIVE) {
+    const int threads = 128;
+    const int64_t grid = (kp.n_list + threads - 1) / threads;
+    if (perm_bits == 16)
+      k_solve_naive<T, uint16_t><<<(unsigned)grid, threads, 0, s>>>(kp);
+    else
+      k_solve_naive<T, uint32_t><<<(unsigned)grid, threads, 0, s>>>(kp);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  const int nslot = nslot_for(max_m);
+  if (nslot < 0 || nslot > max_nslot<T>())
+    return fail(LP2D_ERR_UNSUPPORTED,
+                "max constraint count " + std::to_string(max_m) +
+                    " exceeds the register-resident kernel (fp32 <= 1024, fp64 <= 512)");
+  if (perm_bits == 16) return launch_by_slots<T, uint16_t>(kp, nslot, dev, s);
+  return launch_by_slots<T, uint32_t>(kp, nslot, dev, s);
+}
+
+int validate_common(const lp2d_batch_soa* b, const lp2d_opts* o, const lp2d_out* out) {
+  if (!b || !o || !out) return fail(LP2D_ERR_ARG, "null argument");
+  if (b->n <= 0) return fail(LP2D_ERR_EMPTY_BATCH, "solve_batch: empty batch");
+  if (o->block_width <= 0)
+    return fail(LP2D_ERR_BLOCK_WIDTH, "solve_batch: block width must be positive");
+  if (b->perm_bits != 16 && b->perm_bits != 32)
+    return fail(LP2D_ERR_ARG, "perm_bits must be 16 or 32");
+  if (b->mem != LP2D_MEM_HOST && b->mem != LP2D_MEM_DEVICE)
+    return fail(LP2D_ERR_ARG, "mem must be LP2D_MEM_HOST or LP2D_MEM_DEVICE");
+  if (o->scheduler != LP2D_SCHED_NAIVE && o->scheduler != LP2D_SCHED_BALANCED)
+    return fail(LP2D_ERR_ARG, "unknown scheduler");
+  if (!b->m || !b->offset || !b->ax || !b->ay || !b->b || !b->perm || !b->c || !b->bound_m)
+    return fail(LP2D_ERR_ARG, "null batch array");
+  if (!out->status || !out->x || !out->y || !out->value)
+    return fail(LP2D_ERR_ARG, "null output array");
+  return 0;
+}
+
+template <typename T>
+KParams make_params(const lp2d_opts* o) {
+  KParams kp{};
+  kp.eps_par = (double)(T)o->eps_parallel;
+  kp.eps_feas = (double)(T)o->eps_feas;
+  kp.eps_hi = eps_hi_of<T>(o->eps_parallel);
+  return kp;
+}
+
+// ---- host mode: one shard [lo, hi) on one device ----------------------------
+template <typename T>
+int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out,
+                     int64_t lo, int64_t hi, int64_t max_m) {
+  if (int rc = ensure_device(dev)) return rc;
+  DeviceState& d = g_dev[dev];
+  std::lock_guard<std::mutex> lock(d.mu);
+  CUDA_TRY(cudaSetDevice(dev));
+  const int64_t cnt = hi - lo;
+  const int64_t e0 = b->offset[lo], e1 = b->offset[hi];
+  const int64_t E = e1 - e0;
+  const size_t ps = b->perm_bits / 8;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t off_m = 0;
+  size_t off_offset = off_m + al(sizeof(int32_t) * cnt);
+  size_t off_ax = off_offset + al(sizeof(int64_t) * (cnt + 1));
+  size_t off_ay = off_ax + al(sizeof(T) * E);
+  size_t off_b = off_ay + al(sizeof(T) * E);
+  size_t off_perm = off_b + al(sizeof(T) * E);
+  size_t off_c = off_perm + al(ps * E);
+  size_t off_M = off_c + al(sizeof(T) * 2 * cnt);
+  size_t off_st = off_M + al(sizeof(T) * cnt);
+  size_t off_x = off_st + al(cnt);
+  size_t off_y = off_x + al(sizeof(T) * cnt);
+  size_t off_v = off_y + al(sizeof(T) * cnt);
+  size_t off_pair = off_v + al(sizeof(T) * cnt);
+  size_t off_viol = off_pair + al(sizeof(int32_t) * 2 * cnt);
+  size_t off_wu = off_viol + al(sizeof(uint32_t) * cnt);
+  size_t total = off_wu + al(sizeof(uint64_t) * cnt);
+  if (d.arena_bytes < total) {
+    if (d.arena) CUDA_TRY(cudaFree(d.arena));
+    d.arena = nullptr;
+    d.arena_bytes = 0;
+    CUDA_TRY(cudaMalloc(&d.arena, total));
+    d.arena_bytes = total;
+  }
+  char* A = static_cast<char*>(d.arena);
+  cudaStream_t s = d.stream;
+  std::vector<int64_t> offs(cnt + 1);
+  for (int64_t j = 0; j <= cnt; ++j) offs[j] = b->offset[lo + j] - e0;
+  CUDA_TRY(cudaMemcpyAsync(A + off_m, b->m + lo, sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(A + off_offset, offs.data(), sizeof(int64_t) * (cnt + 1),
+                           cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(A + off_ax, static_cast<const T*>(b->ax) + e0, sizeof(T) * E,
+                           cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(A + off_ay, static_cast<const T*>(b->ay) + e0, sizeof(T) * E,
+                           cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(A + off_b, static_cast<const T*>(b->b) + e0, sizeof(T) * E,
+                           cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(A + off_perm, static_cast<const char*>(b->perm) + ps * e0, ps * E,
+                           cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(A + off_c, static_cast<const T*>(b->c) + 2 * lo, sizeof(T) * 2 * cnt,
+                           cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(A + off_M, static_cast<const T*>(b->bound_m) + lo, sizeof(T) * cnt,
+                           cudaMemcpyHostToDevice, s));
+  KParams kp = make_params<T>(o);
+  kp.n_list = cnt;
+  kp.list = nullptr;
+  kp.m = reinterpret_cast<const int32_t*>(A + off_m);
+  kp.offset = reinterpret_cast<const int64_t*>(A + off_offset);
+  kp.ax = A + off_ax;
+  kp.ay = A + off_ay;
+  kp.b = A + off_b;
+  kp.perm = A + off_perm;
+  kp.c = A + off_c;
+  kp.bound_m = A + off_M;
+  kp.status = reinterpret_cast<uint8_t*>(A + off_st);
+  kp.x = A + off_x;
+  kp.y = A + off_y;
+  kp.value = A + off_v;
+  kp.pair = reinterpret_cast<int32_t*>(A + off_pair);
+  kp.viol = reinterpret_cast<uint32_t*>(A + off_viol);
+  kp.wu = reinterpret_cast<uint64_t*>(A + off_wu);
+  if (int rc = launch_solve<T>(kp, max_m, b->perm_bits, o->scheduler, dev, s)) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out->status + lo, A + off_st, cnt, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(static_cast<T*>(out->x) + lo, A + off_x, sizeof(T) * cnt,
+                           cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(static_cast<T*>(out->y) + lo, A + off_y, sizeof(T) * cnt,
+                           cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(static_cast<T*>(out->value) + lo, A + off_v, sizeof(T) * cnt,
+                           cudaMemcpyDeviceToHost, s));
+  if (out->pair)
+    CUDA_TRY(cudaMemcpyAsync(out->pair + 2 * lo, A + off_pair, sizeof(int32_t) * 2 * cnt,
+                             cudaMemcpyDeviceToHost, s));
+  if (out->violation_events)
+    CUDA_TRY(cudaMemcpyAsync(out->violation_events + lo, A + off_viol, sizeof(uint32_t) * cnt,
+                             cudaMemcpyDeviceToHost, s));
+  if (out->work_units)
+    CUDA_TRY(cudaMemcpyAsync(out->work_units + lo, A + off_wu, sizeof(uint64_t) * cnt,
+                             cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return 0;
+}
+
+template <typename T>
+int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
+  if (int rc = validate_common(b, o, out)) return rc;
+  DeviceGuard guard;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(LP2D_ERR_CUDA, "no CUDA device visible (the solver has no CPU fallback)");
+  if (b->mem == LP2D_MEM_DEVICE) {
+    if (b->max_m < 0) return fail(LP2D_ERR_ARG, "device mode needs max_m");
+    if (b->perm_bits == 16 && b->max_m > 65536)
+      return fail(LP2D_ERR_ARG, "u16 permutations need m <= 65536");
+    const int dev = o->device;
+    if (dev < 0 || dev >= ndev) return fail(LP2D_ERR_ARG, "bad device ordinal");
+    if (int rc = ensure_device(dev)) return rc;
+    CUDA_TRY(cudaSetDevice(dev));
+    KParams kp = make_params<T>(o);
+    kp.n_list = b->n;
+    kp.m = b->m;
+    kp.offset = b->offset;
+    kp.ax = b->ax;
+    kp.ay = b->ay;
+    kp.b = b->b;
+    kp.perm = b->perm;
+    kp.c = b->c;
+    kp.bound_m = b->bound_m;
+    kp.status = out->status;
+    kp.x = out->x;
+    kp.y = out->y;
+    kp.value = out->value;
+    kp.pair = out->pair;
+    kp.viol = out->violation_events;
+    kp.wu = out->work_units;
+    return launch_solve<T>(kp, b->max_m, b->perm_bits, o->scheduler, dev,
+                           static_cast<cudaStream_t>(o->stream));
+  }
+  // host mode: validate the layout contract, then shard.
+  int64_t max_m = 0;
+  for (int64_t j = 0; j < b->n; ++j) {
+    const int64_t mj = b->m[j];
+    if (mj < 0) return fail(LP2D_ERR_PERM_LENGTH, "negative constraint count");
+    const int64_t cap8 = (mj + 7) & ~int64_t(7);
+    if ((b->offset[j] & 7) != 0 || b->offset[j + 1] - b->offset[j] < cap8)
+      return fail(LP2D_ERR_LAYOUT, "offset[" + std::to_string(j) +
+                                       "] violates the 8-element layout contract");
+    max_m = std::max(max_m, mj);
+  }
+  if (b->perm_bits == 16 && max_m > 65536)
+    return fail(LP2D_ERR_ARG, "u16 permutations need m <= 65536");
+  int use = o->n_gpus > 0 ? std::min(o->n_gpus, ndev) : ndev;
+  use = (int)std::min<int64_t>(use, b->n);
+  // Contiguous LP ranges balanced by sum(m + 4).
+  std::vector<int64_t> cut(use + 1, 0);
+  cut[use] = b->n;
+  if (use > 1) {
+    double total = 0;
+    for (int64_t j = 0; j < b->n; ++j) total += (double)b->m[j] + 4.0;
+    double acc = 0;
+    int k = 1;
+    for (int64_t j = 0; j < b->n && k < use; ++j) {
+      acc += (double)b->m[j] + 4.0;
+      while (k < use && acc >= total * k / use) cut[k++] = j + 1;
+    }
+    for (; k < use; ++k) cut[k] = b->n;
+  }
+  if (use == 1) return solve_shard_host<T>(0, b, o, out, 0, b->n, max_m);
+  std::vector<int> rcs(use, 0);
+  std::vector<std::string> errs(use);
+  std::vector<std::thread> th;
+  for (int g = 0; g < use; ++g) {
+    th.emplace_back([&, g] {
+      if (cut[g + 1] > cut[g]) rcs[g] = solve_shard_host<T>(g, b, o, out, cut[g], cut[g + 1], max_m);
+      if (rcs[g]) errs[g] = g_err;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int g = 0; g < use; ++g)
+    if (rcs[g]) return fail(rcs[g], "device " + std::to_string(g) + ": " + errs[g]);
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+void lp2dgpu_default_opts(lp2d_opts* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->scheduler = LP2D_SCHED_BALANCED;
+  o->block_width = 512;
+  o->eps_parallel = 1e-12;
+  o->eps_feas = 1e-9;
+}
+
+int lp2dgpu_solve_f32(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
+  return solve_impl<float>(b, o, out);
+}
+
+int lp2dgpu_solve_f64(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
+  return solve_impl<double>(b, o, out);
+}
+
+int64_t lp2dgpu_pack_offsets(int64_t n, const int32_t* m, int64_t* offset) {
+  int64_t acc = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    offset[j] = acc;
+    acc += ((int64_t)std::max(m[j], 0) + 7) & ~int64_t(7);
+  }
+  offset[n] = acc;
+  return acc;
+}
+
+int lp2dgpu_shuffle_device(int64_t n, const int32_t* m, const int64_t* offset,
+                           const uint64_t* seeds, void* perm, int32_t perm_bits,
+                           int32_t device, void* stream) {
+  if (n <= 0) return 0;
+  if (!m || !offset || !seeds || !perm) return fail(LP2D_ERR_ARG, "null argument");
+  DeviceGuard guard;
+  if (int rc = ensure_device(device)) return rc;
+  CUDA_TRY(cudaSetDevice(device));
+  const int threads = 128;
+  const unsigned grid = (unsigned)((n + threads - 1) / threads);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (perm_bits == 16)
+    k_shuffle<uint16_t><<<grid, threads, 0, s>>>(n, m, offset, seeds, static_cast<uint16_t*>(perm));
+  else if (perm_bits == 32)
+    k_shuffle<uint32_t><<<grid, threads, 0, s>>>(n, m, offset, seeds, static_cast<uint32_t*>(perm));
+  else
+    return fail(LP2D_ERR_ARG, "perm_bits must be 16 or 32");
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int lp2dgpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+const char* lp2dgpu_last_error(void) { return g_err.c_str(); }
+
+const char* lp2dgpu_version(void) {
+  return "lp2d_b200 0.1 (sm_100a; warp-register Seidel/RGB, TMA bulk prefetch)";
+}
+
+}  // extern "C"
