@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "liblp2d_b200.so")
+# LP2D_B200_LIB overrides the in-tree build (A/B experiments of kernel variants).
+LIB_PATH = os.environ.get("LP2D_B200_LIB", os.path.join(_HERE, "lib", "liblp2d_b200.so"))
 CSRC = os.path.join(_HERE, "csrc")
 
 # include/lp2d_b200.h

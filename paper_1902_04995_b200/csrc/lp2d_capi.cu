@@ -82,19 +82,18 @@ uint32_t* take_counter(int dev) {
   return d.counters + 2 * s;
 }
 
+// Register slot classes: NS slots hold m + 4 positions (box included).
+constexpr int kSlotClasses[] = {1, 2, 3, 5, 9, 17, 33};
+
 int nslot_for(int64_t max_m) {
-  if (max_m <= 32) return 1;
-  if (max_m <= 64) return 2;
-  if (max_m <= 128) return 4;
-  if (max_m <= 256) return 8;
-  if (max_m <= 512) return 16;
-  if (max_m <= 1024) return 32;
+  for (int ns : kSlotClasses)
+    if (max_m + 4 <= 32 * ns) return ns;
   return -1;
 }
 
 template <typename T>
 constexpr int max_nslot() {
-  return sizeof(T) == 4 ? 32 : 16;  // fp64 keeps m <= 512 in registers
+  return sizeof(T) == 4 ? 33 : 17;  // fp64 keeps m <= 540 in registers
 }
 
 // Eps_par rounded up by 2^-10 (relative), in T: the parallel-filter factor.
@@ -135,11 +134,12 @@ int launch_by_slots(const KParams& kp, int nslot, int dev, cudaStream_t s) {
   switch (nslot) {
     case 1: return launch_warp_kernel<T, P, 1>(kp, dev, s);
     case 2: return launch_warp_kernel<T, P, 2>(kp, dev, s);
-    case 4: return launch_warp_kernel<T, P, 4>(kp, dev, s);
-    case 8: return launch_warp_kernel<T, P, 8>(kp, dev, s);
-    case 16: return launch_warp_kernel<T, P, 16>(kp, dev, s);
-    case 32:
-      if constexpr (max_nslot<T>() >= 32) return launch_warp_kernel<T, P, 32>(kp, dev, s);
+    case 3: return launch_warp_kernel<T, P, 3>(kp, dev, s);
+    case 5: return launch_warp_kernel<T, P, 5>(kp, dev, s);
+    case 9: return launch_warp_kernel<T, P, 9>(kp, dev, s);
+    case 17: return launch_warp_kernel<T, P, 17>(kp, dev, s);
+    case 33:
+      if constexpr (max_nslot<T>() >= 33) return launch_warp_kernel<T, P, 33>(kp, dev, s);
       break;
   }
   return fail(LP2D_ERR_UNSUPPORTED, "constraint count above the register-resident size classes");
@@ -163,7 +163,7 @@ int launch_solve(const KParams& kp, int64_t max_m, int perm_bits, int sched, int
   if (nslot < 0 || nslot > max_nslot<T>())
     return fail(LP2D_ERR_UNSUPPORTED,
                 "max constraint count " + std::to_string(max_m) +
-                    " exceeds the register-resident kernel (fp32 <= 1024, fp64 <= 512)");
+                    " exceeds the register-resident kernel (fp32 <= 1052, fp64 <= 540)");
   if (perm_bits == 16) return launch_by_slots<T, uint16_t>(kp, nslot, dev, s);
   return launch_by_slots<T, uint32_t>(kp, nslot, dev, s);
 }
@@ -192,6 +192,9 @@ KParams make_params(const lp2d_opts* o) {
   kp.eps_par = (double)(T)o->eps_parallel;
   kp.eps_feas = (double)(T)o->eps_feas;
   kp.eps_hi = eps_hi_of<T>(o->eps_parallel);
+  kp.eps_par_f = (float)kp.eps_par;
+  kp.eps_feas_f = (float)kp.eps_feas;
+  kp.eps_hi_f = (float)kp.eps_hi;
   return kp;
 }
 

@@ -47,21 +47,45 @@ struct KParams {
   uint32_t* viol;
   uint64_t* wu;
   uint32_t* counter;     // [0] LP ticket, [1] finished warps (self-resetting)
-  double eps_par, eps_feas, eps_hi;
+  double eps_par, eps_feas, eps_hi;   // tolerance rounded to the scalar type
+  float eps_par_f, eps_feas_f, eps_hi_f;  // (float copies: constant-bank operands)
   int32_t total_warps;
+};
+
+template <typename T>
+struct Eps {
+  static __device__ __forceinline__ T par(const KParams& p) { return (T)p.eps_par; }
+  static __device__ __forceinline__ T feas(const KParams& p) { return (T)p.eps_feas; }
+  static __device__ __forceinline__ T hi(const KParams& p) { return (T)p.eps_hi; }
+};
+template <>
+struct Eps<float> {
+  static __device__ __forceinline__ float par(const KParams& p) { return p.eps_par_f; }
+  static __device__ __forceinline__ float feas(const KParams& p) { return p.eps_feas_f; }
+  static __device__ __forceinline__ float hi(const KParams& p) { return p.eps_hi_f; }
 };
 
 __host__ __device__ constexpr uint32_t round16(uint32_t x) {
   return (x + 15u) & ~15u;
 }
 
-template <typename T, typename P, int NSLOT>
+// Register-resident layout: NS slots of 32 lanes hold considered positions
+// P = 32*slot + lane, P in [0, m+4): positions 0..3 are the box constraints
+// (serial.hpp:47-52), P >= 4 is user constraint perm[P-4] (batch.hpp:137-139).
+// The staging buffer holds one LP of up to kCap = 32*NS-4 constraints.
+template <typename T, typename P, int NS>
 struct WarpLayout {
-  static constexpr int kCap = 32 * NSLOT;
+  static constexpr int kCap = 32 * NS - 4;
   static constexpr uint32_t kArr = round16(kCap * sizeof(T));
   static constexpr uint32_t kPerm = round16(kCap * sizeof(P));
   static constexpr uint32_t kBuf = 3 * kArr + kPerm;  // per warp
   static constexpr uint32_t kSmem = kWarpsPerCta * kBuf + kWarpsPerCta * 8;
+  // Occupancy target: 3 CTAs (12 warps) per SM for the big classes.
+#ifndef LP2D_MIN_BLOCKS
+#define LP2D_MIN_BLOCKS 3
+#endif
+  static constexpr int kMinBlocks =
+      (LP2D_MIN_BLOCKS * kBuf * kWarpsPerCta <= 220 * 1024) ? LP2D_MIN_BLOCKS : 2;
 };
 
 // Per-LP header held by lane 0 between claim and solve.
@@ -74,11 +98,11 @@ struct Header {
   T cx, cy, M;
 };
 
-template <typename T, typename P, int NSLOT>
+template <typename T, typename P, int NS>
 __device__ __forceinline__ void issue_lp(const KParams& p, int64_t j,
                                          unsigned char* buf, uint64_t* bar,
                                          uint64_t policy, Header<T>& h) {
-  using L = WarpLayout<T, P, NSLOT>;
+  using L = WarpLayout<T, P, NS>;
   const int64_t lp = p.list ? (int64_t)p.list[j] : j;
   const int32_t mj = p.m[lp];
   const int64_t o = p.offset[lp];
@@ -151,10 +175,169 @@ __device__ __forceinline__ void write_result(const KParams& p,
   if (p.wu) p.wu[lp] = wu;
 }
 
-template <typename T, typename P, int NSLOT>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+// Exact 1D fold over considered positions [0, pi) straight from global
+// memory with the reference's classify (wu_apply). Taken only when a unit of
+// the register fold hit the parallel bound (essentially parallel constraints),
+// so speed is irrelevant; out of line to keep the hot code small.
+template <typename T, typename P>
+__device__ __noinline__ Acc<T> fold_exact_global(const KParams& p, int64_t off,
+                                                 uint32_t pi, Line<T> l, T M,
+                                                 T eps_par, T eps_feas, T eps_hi) {
+  const int lane = threadIdx.x & 31;
+  const T* ax = static_cast<const T*>(p.ax) + off;
+  const T* ay = static_cast<const T*>(p.ay) + off;
+  const T* b = static_cast<const T*>(p.b) + off;
+  const P* perm = static_cast<const P*>(p.perm) + off;
+  Acc<T> acc;
+  acc.uL = -T(INFINITY);
+  acc.uR = T(INFINITY);
+  acc.oL = acc.oR = acc.par = kNone;
+  for (uint32_t k = lane; k < pi; k += 32) {
+    T vax, vay, vb;
+    if (k < 4) {
+      vax = k == 0 ? T(1) : (k == 1 ? T(-1) : T(0));
+      vay = k == 2 ? T(1) : (k == 3 ? T(-1) : T(0));
+      vb = M;
+    } else {
+      const uint32_t o = perm[k - 4];
+      vax = ax[o];
+      vay = ay[o];
+      vb = b[o];
+    }
+    wu_apply(vax, vay, vb, l, eps_par, eps_feas, eps_hi, k, acc);
+  }
+  return acc;
+}
+
+// Per-LP running state of the incremental loop (serial.hpp:159-188) plus the
+// builder's defining pair (considered positions) and the solve_stats.
+template <typename T>
+struct LPState {
+  T px, py;
+  uint32_t pos0, pos1;
+  uint32_t viol;
+  uint64_t wu;
+  uint8_t st;  // 0 running/optimal, 1 infeasible, 255 invalid
+};
+
+template <typename T>
+__device__ __forceinline__ void lp_init(LPState<T>& S, const Header<T>& h) {
+  const T M = h.M;
+  S.px = h.cx < T(0) ? -M : M;  // serial.hpp:56-58
+  S.py = h.cy < T(0) ? -M : M;
+  S.pos0 = h.cx < T(0) ? 1u : 0u;  // the box corner's two edges
+  S.pos1 = h.cy < T(0) ? 3u : 2u;
+  S.viol = 0;
+  S.wu = 0;
+  S.st = 0;
+}
+
+// Merge the lanes' folded intervals and resolve the 1D program on l
+// (serial.hpp:95-111), for the violation at considered position pi. Returns
+// false when the LP turned out infeasible (S.st = 1).
+template <typename T>
+__device__ __forceinline__ bool resolve_event(LPState<T>& S, const Acc<T>& acc,
+                                              const Line<T>& l, uint32_t pi,
+                                              const Header<T>& h, T cthr,
+                                              T eps_feas) {
+  const uint32_t par = __reduce_min_sync(kFull, acc.par);
+  if (par != kNone) {  // serial.hpp:97 parallel-infeasible
+    S.st = 1;
+    S.pos0 = pi;
+    S.pos1 = par;
+    return false;
+  }
+  T uL, nuR;
+  uint32_t oL, oR;
+  warp_best(acc.uL, acc.oL, uL, oL);
+  warp_best(-acc.uR, acc.oR, nuR, oR);
+  const T uR = -nuR;
+  const T scale = fmax(fabs(uL), fabs(uR));
+  if (uL > uR + feas_slack(eps_feas, scale)) {  // serial.hpp:98-101
+    S.st = 1;
+    S.pos0 = pi;
+    S.pos1 = oL;
+    return false;
+  }
+  const T along = h.cx * l.dx + h.cy * l.dy;  // serial.hpp:102-108
+  const bool take_right = !(fabs(along) <= cthr) && along > T(0);
+  const T t = take_right ? uR : uL;
+  S.px = l.ox + t * l.dx;
+  S.py = l.oy + t * l.dy;
+  S.pos0 = pi;
+  S.pos1 = take_right ? oR : oL;
+  return true;
+}
+
+// Whole-LP exact solve straight from global memory (no register staging):
+// the reference loop with warp-parallel tests and folds. Used for LPs whose
+// magnitudes leave the fast path's proven range (non-finite or huge
+// coefficients, a non-finite running optimum); rare, so simple.
+template <typename T, typename P>
+__device__ __noinline__ void solve_exact_global(const KParams& p, const Header<T>& h,
+                                                T eps_par, T eps_feas, T eps_hi,
+                                                LPState<T>& S) {
+  const int lane = threadIdx.x & 31;
+  const T* ax = static_cast<const T*>(p.ax) + h.off;
+  const T* ay = static_cast<const T*>(p.ay) + h.off;
+  const T* b = static_cast<const T*>(p.b) + h.off;
+  const P* perm = static_cast<const P*>(p.perm) + h.off;
+  lp_init(S, h);
+  const T cthr = eps_par * sqrt(h.cx * h.cx + h.cy * h.cy);
+  const int m = h.m;
+  int start = 0;
+  while (start < m) {
+    const int i = start + lane;
+    bool v = false;
+    if (i < m) {
+      const uint32_t o = perm[i];
+      v = !satisfied(ax[o], ay[o], b[o], S.px, S.py, eps_feas);
+    }
+    const uint32_t vm = __ballot_sync(kFull, v);
+    if (!vm) {
+      start += 32;
+      continue;
+    }
+    const int iv = start + __ffs(vm) - 1;
+    const uint32_t o = perm[iv];
+    const uint32_t pi = 4u + (uint32_t)iv;
+    S.viol += 1;
+    S.wu += pi;
+    const Line<T> l = boundary_of(ax[o], ay[o], b[o]);
+    const Acc<T> acc = fold_exact_global<T, P>(p, h.off, pi, l, h.M, eps_par, eps_feas, eps_hi);
+    if (!resolve_event(S, acc, l, pi, h, cthr, eps_feas)) return;
+    start = iv + 1;
+  }
+}
+
+// One case of the violation-test dispatch: test slot K (compile-time) against
+// the current optimum; on the first violated lane leave the switch with
+// sfound = K. Entering the switch at `case s` resumes the sweep where the
+// previous event left it (Duff's device), so no code runs for earlier slots.
+#define LP2D_TEST_CASE(K)                                                   \
+  case K:                                                                   \
+    if constexpr (K < NS) {                                                 \
+      if (32 * K >= mpos) break;                                            \
+      const bool v = !satisfied(rax[K], ray[K], rb[K], px, py, eps_feas);   \
+      uint32_t vm = __ballot_sync(kFull, v) & startmask;                    \
+      startmask = kFull;                                                    \
+      hx = opaque_copy(rax[K]);                                             \
+      hy = opaque_copy(ray[K]);                                             \
+      hb = opaque_copy(rb[K]);                                              \
+      if (vm) {                                                             \
+        vfound = vm;                                                        \
+        sfound = K;                                                         \
+        break;                                                              \
+      }                                                                     \
+    }                                                                       \
+    [[fallthrough]];
+
+template <typename T, typename P, int NS>
+__global__ void __launch_bounds__(kWarpsPerCta * 32,
+                                  (WarpLayout<T, P, NS>::kMinBlocks))
     k_solve_warp(const KParams p) {
-  using L = WarpLayout<T, P, NSLOT>;
+  static_assert(NS >= 1 && NS <= 40, "slot count");
+  using L = WarpLayout<T, P, NS>;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wic = threadIdx.x >> 5;
@@ -165,9 +348,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   const T* sb = reinterpret_cast<const T*>(buf + 2 * L::kArr);
   const P* sperm = reinterpret_cast<const P*>(buf + 3 * L::kArr);
 
-  const T eps_par = (T)p.eps_par;
-  const T eps_feas = (T)p.eps_feas;
-  const T eps_hi = (T)p.eps_hi;
+  const T eps_par = Eps<T>::par(p);
+  const T eps_feas = Eps<T>::feas(p);
+  const T eps_hi = Eps<T>::hi(p);
   const uint64_t policy = policy_evict_first();
 
   if (lane == 0) mbar_init(bar, 1);
@@ -176,151 +359,135 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   uint32_t phase = 0;
   int64_t j = (int64_t)blockIdx.x * kWarpsPerCta + wic;
   Header<T> hn{};
-  if (lane == 0 && j < p.n_list) issue_lp<T, P, NSLOT>(p, j, buf, bar, policy, hn);
-
-  // Box constraint folded by this lane at every event (positions 0..3,
-  // serial.hpp:47-52); lanes 4..31 duplicate one of them harmlessly.
-  const int bk = lane & 3;
-  const T bax = bk == 0 ? T(1) : (bk == 1 ? T(-1) : T(0));
-  const T bay = bk == 2 ? T(1) : (bk == 3 ? T(-1) : T(0));
+  if (lane == 0 && j < p.n_list) issue_lp<T, P, NS>(p, j, buf, bar, policy, hn);
 
   while (j < p.n_list) {
     const Header<T> h = bcast(hn);
     mbar_wait(bar, phase);
     phase ^= 1u;
 
-    // ---- gather the LP into registers in insertion order ------------------
-    T rax[NSLOT], ray[NSLOT], rb[NSLOT];
-    bool bad = !h.ok;
+    // ---- gather: positions P = 32*K + lane in insertion order ---------------
+    // Out-of-range perm entries are clamped for the load and reported through
+    // pmax (status LP2D_INVALID). sbits tracks max |ax|+|ay| as float bits,
+    // which orders NaN/INF above every finite value.
+    T rax[NS], ray[NS], rb[NS];
     const int mj = h.ok ? h.m : 0;
+    const int mpos = mj + 4;
+    uint32_t pmax = 0;
+    decltype(float_bits(T(0))) sbits = 0;
 #pragma unroll
-    for (int s = 0; s < NSLOT; ++s) {
-      const int k = 32 * s + lane;
-      T vax = T(0), vay = T(0), vb = T(0);
-      if (k < mj) {
-        uint32_t o = sperm[k];
-        if (o >= (uint32_t)mj) {
-          bad = true;
-          o = 0;
-        }
-        vax = sax[o];
-        vay = say[o];
-        vb = sb[o];
+    for (int K = 0; K < NS; ++K) {
+      const int P_ = 32 * K + lane;
+      // padding positions (>= m+4) never violate: 0*px + 0*py <= +INF
+      T vax = T(0), vay = T(0), vb = T(INFINITY);
+      if (K == 0 && P_ < 4) {
+        vax = P_ == 0 ? T(1) : (P_ == 1 ? T(-1) : T(0));
+        vay = P_ == 2 ? T(1) : (P_ == 3 ? T(-1) : T(0));
+        vb = h.M;
+      } else if (P_ < mpos) {
+        const uint32_t o = sperm[P_ - 4];
+        pmax = max(pmax, o);
+        const uint32_t oc = min(o, (uint32_t)(L::kCap - 1));
+        vax = sax[oc];
+        vay = say[oc];
+        vb = sb[oc];
+        sbits = max(sbits, float_bits(fabs(vax) + fabs(vay)));
       }
-      rax[s] = vax;
-      ray[s] = vay;
-      rb[s] = vb;
+      rax[K] = vax;
+      ray[K] = vay;
+      rb[K] = vb;
     }
-    bad = __any_sync(kFull, bad);
+    const bool bad = !h.ok || (mj > 0 && __reduce_max_sync(kFull, pmax) >= (uint32_t)mj);
     __syncwarp();
     fence_proxy_async_smem();
 
-    // ---- claim + prefetch the next LP (overlaps this LP's solve) ----------
+    // ---- claim + prefetch the next LP (overlaps this LP's solve) ------------
     int64_t jn = 0;
     if (lane == 0) jn = (int64_t)atomicAdd(p.counter, 1u) + p.total_warps;
     jn = __shfl_sync(kFull, jn, 0);
-    if (lane == 0 && jn < p.n_list) issue_lp<T, P, NSLOT>(p, jn, buf, bar, policy, hn);
+    if (lane == 0 && jn < p.n_list) issue_lp<T, P, NS>(p, jn, buf, bar, policy, hn);
 
-    // ---- solve (serial.hpp:159-188) ---------------------------------------
-    const T M = h.M;
-    T px = h.cx < T(0) ? -M : M;  // serial.hpp:56-58
-    T py = h.cy < T(0) ? -M : M;
-    uint32_t pos0 = h.cx < T(0) ? 1u : 0u;
-    uint32_t pos1 = h.cy < T(0) ? 3u : 2u;
+    // Per-LP parallel-test bound (see wu_fold), never below the fast
+    // division's divisor floor. LPs outside the proven range go to the exact
+    // global-memory solver.
+    const T m_all = float_from_bits<T>(reduce_max_bits(sbits));
+    bool wild = !(m_all < Limits<T>::kBig) || !(fabs(h.M) < T(INFINITY));
+    const T lpbnd = fmax(fmax(fmax(m_all, T(1)), Limits<T>::kSmall) * eps_hi,
+                         FastDiv<T>::kDLo);
+
+    // ---- solve (serial.hpp:159-188) -----------------------------------------
+    LPState<T> S;
+    lp_init(S, h);
+    S.st = bad ? 255 : 0;
     const T cthr = eps_par * sqrt(h.cx * h.cx + h.cy * h.cy);
-    uint32_t viol = 0;
-    uint64_t wu = 0;
-    uint8_t st = bad ? 255 : 0;
     int s = 0;
-    uint32_t startmask = kFull;
-    while (!bad) {
+    uint32_t startmask = 0xfffffff0u;  // the box is never tested
+    bool running = !bad && !wild;
+    while (running) {
       // Speculative chunked violation test from slot s onward.
-      bool ev = false;
-      int f = 0;
+      const T px = S.px, py = S.py;
+      int sfound = -1;
+      uint32_t vfound = 0;
       T hx = T(0), hy = T(0), hb = T(0);
-#pragma unroll
-      for (int S = 0; S < NSLOT; ++S) {
-        if (S < s) continue;
-        if (32 * S >= mj) break;
-        const bool v = (32 * S + lane < mj) &&
-                       !satisfied(rax[S], ray[S], rb[S], px, py, eps_feas);
-        const uint32_t vm = __ballot_sync(kFull, v) & startmask;
-        startmask = kFull;
-        // Unconditional opaque copies (not a shuffle inside the branch): the
-        // compiler cannot merge them into one dynamically indexed load after
-        // the loop, so the slot index stays compile-time and the arrays stay
-        // in registers.
-        hx = opaque_copy(rax[S]);
-        hy = opaque_copy(ray[S]);
-        hb = opaque_copy(rb[S]);
-        if (vm) {
-          f = __ffs(vm) - 1;
-          s = S;
-          ev = true;
+      switch (s) {
+        LP2D_TEST_CASE(0) LP2D_TEST_CASE(1) LP2D_TEST_CASE(2) LP2D_TEST_CASE(3)
+        LP2D_TEST_CASE(4) LP2D_TEST_CASE(5) LP2D_TEST_CASE(6) LP2D_TEST_CASE(7)
+        LP2D_TEST_CASE(8) LP2D_TEST_CASE(9) LP2D_TEST_CASE(10) LP2D_TEST_CASE(11)
+        LP2D_TEST_CASE(12) LP2D_TEST_CASE(13) LP2D_TEST_CASE(14) LP2D_TEST_CASE(15)
+        LP2D_TEST_CASE(16) LP2D_TEST_CASE(17) LP2D_TEST_CASE(18) LP2D_TEST_CASE(19)
+        LP2D_TEST_CASE(20) LP2D_TEST_CASE(21) LP2D_TEST_CASE(22) LP2D_TEST_CASE(23)
+        LP2D_TEST_CASE(24) LP2D_TEST_CASE(25) LP2D_TEST_CASE(26) LP2D_TEST_CASE(27)
+        LP2D_TEST_CASE(28) LP2D_TEST_CASE(29) LP2D_TEST_CASE(30) LP2D_TEST_CASE(31)
+        LP2D_TEST_CASE(32) LP2D_TEST_CASE(33) LP2D_TEST_CASE(34) LP2D_TEST_CASE(35)
+        LP2D_TEST_CASE(36) LP2D_TEST_CASE(37) LP2D_TEST_CASE(38) LP2D_TEST_CASE(39)
+        default:
           break;
-        }
       }
-      if (!ev) break;
+      if (sfound < 0) break;
+      // Launder the slot so the work-unit loop below is one shared copy, not
+      // specialised per dispatch exit.
+      s = opaque_int(sfound);
+
+      // Violation at position pi = 4 + i: 1D LP over positions 0..pi-1.
+      // (Copies + one shuffle after the dispatch, not a shuffle per case:
+      // keeps every case a few instructions and the arrays in registers.)
+      const int f = __ffs(vfound) - 1;
       hx = __shfl_sync(kFull, hx, f);
       hy = __shfl_sync(kFull, hy, f);
       hb = __shfl_sync(kFull, hb, f);
-
-      // Violation at insertion index i: 1D LP over positions 0..i+3.
-      const uint32_t i = 32u * (uint32_t)s + (uint32_t)f;
-      viol += 1;
-      wu += 4 + i;
+      const uint32_t pi = 32u * (uint32_t)s + (uint32_t)f;
+      S.viol += 1;
+      S.wu += pi;  // considered.size() (serial.hpp:176-179)
       const Line<T> l = boundary_of(hx, hy, hb);
       Acc<T> acc;
       acc.uL = -T(INFINITY);
       acc.uR = T(INFINITY);
       acc.oL = acc.oR = acc.par = kNone;
-      wu_apply(bax, bay, M, l, eps_par, eps_feas, eps_hi, (uint32_t)bk, acc);
+      bool rare = false;
 #pragma unroll
-      for (int S = 0; S < NSLOT; ++S) {
-        if (S > s) break;
-        const uint32_t k = 32u * S + lane;
-        if (k < i) wu_apply(rax[S], ray[S], rb[S], l, eps_par, eps_feas, eps_hi, 4u + k, acc);
+      for (int K = 0; K < NS; ++K) {
+        const uint32_t k = 32u * K + lane;
+        wu_fold(rax[K], ray[K], rb[K], l, lpbnd, k, k < pi, acc, rare);
+        if (K >= s) break;
       }
-      const uint32_t par = __reduce_min_sync(kFull, acc.par);
-      if (par != kNone) {  // serial.hpp:97 parallel-infeasible
-        st = 1;
-        pos0 = 4 + i;
-        pos1 = par;
+      if (__any_sync(kFull, rare))
+        acc = fold_exact_global<T, P>(p, h.off, pi, l, h.M, eps_par, eps_feas, eps_hi);
+      if (!resolve_event(S, acc, l, pi, h, cthr, eps_feas)) break;
+      if (!(fabs(S.px) < T(INFINITY) && fabs(S.py) < T(INFINITY))) {
+        wild = true;  // the padding test needs a finite optimum
         break;
       }
-      T uL, nuR;
-      uint32_t oL, oR;
-      warp_best(acc.uL, acc.oL, uL, oL);
-      warp_best(-acc.uR, acc.oR, nuR, oR);
-      const T uR = -nuR;
-      const T scale = fmax(fabs(uL), fabs(uR));
-      if (uL > uR + feas_slack(eps_feas, scale)) {  // serial.hpp:98-101
-        st = 1;
-        pos0 = 4 + i;
-        pos1 = oL;
-        break;
-      }
-      const T along = h.cx * l.dx + h.cy * l.dy;
-      T t;
-      uint32_t own;
-      if (fabs(along) <= cthr) {
-        t = uL;
-        own = oL;
-      } else if (along > T(0)) {
-        t = uR;
-        own = oR;
+      if (f == 31) {
+        s += 1;
+        startmask = kFull;
       } else {
-        t = uL;
-        own = oL;
+        startmask = kFull << (f + 1);
       }
-      px = l.ox + t * l.dx;
-      py = l.oy + t * l.dy;
-      pos0 = 4 + i;
-      pos1 = own;
-      startmask = (f == 31) ? 0u : (kFull << (f + 1));
     }
-    if (st == 0 && (pos0 < 4 || pos1 < 4)) st = 2;
-    if (lane == 0) write_result<T, P>(p, h, st, px, py, pos0, pos1, viol, wu);
+    if (wild && !bad) solve_exact_global<T, P>(p, h, eps_par, eps_feas, eps_hi, S);
+    uint8_t st = S.st;
+    if (st == 0 && (S.pos0 < 4 || S.pos1 < 4)) st = 2;
+    if (lane == 0) write_result<T, P>(p, h, st, S.px, S.py, S.pos0, S.pos1, S.viol, S.wu);
     j = jn;
   }
 
@@ -335,6 +502,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     }
   }
 }
+#undef LP2D_TEST_CASE
 
 // Naive: thread per LP, the serial loop with global-memory gathers.
 template <typename T, typename P>
