@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark of the batch 2D-LP solve path (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+                  [--impl ours|reference]
+
+A step is one solve of the whole per-GPU batch. Default workload (configs[1]
+of BASELINE.json): 16384 LPs x 1024 constraints, fp32, synthesised with the
+reference's own generator streams (gen_mixed, seed 2; LP j of the global
+batch is seeded by its global index, so shards are reproducible).
+
+Under torchrun (N > 1) every rank solves its own 16384-LP shard of an
+N*16384-LP global batch ("scaling": "weak"); LPs are independent, so there is
+no data-path collective — only a barrier and a MAX all-reduce of the timings.
+
+value     : LPs/s, kernel on device-resident inputs, CUDA events on the
+            launching stream, K steps bracketed by barrier + synchronize.
+e2e       : LPs/s through the C ABI with pinned HOST buffers (H2D of every
+            input and D2H of every output inside the timed region).
+roofline  : algorithmic bytes 3*sizeof(T)*m per LP over
+            the kernel's average event-timed duration, against the measured
+            HBM copy bandwidth in MEASURED_PEAKS.json.
+cpu_baseline / --impl reference : the unmodified reference (oracle/_ref, the
+            reference headers compiled by oracle/Makefile) timed on this
+            box's host cores — solve_batch(balanced, width 512, workers = all
+            hardware threads) on the same instances, in fp64 (the reference
+            has no fp32 path; fp32 configs feed it the fp32-rounded inputs).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LPs solved/sec at 16384 LPs x 1024 constraints; achieved HBM GB/s vs peak"
+
+CONFIGS = {
+    # name: (per-GPU LPs, m, dtype, seed, description)
+    "c1": (1024, 64, np.float32, 1, "1024 LPs x 64 constraints fp32 (BASELINE configs[0])"),
+    "c2": (16384, 1024, np.float32, 2, "16384 LPs x 1024 constraints fp32 (BASELINE configs[1])"),
+    "c3": (1 << 17, 128, np.float32, 3, "2^20 LPs x 128 constraints fp32 sharded over 8 GPUs: 2^17 per GPU (BASELINE configs[2])"),
+    "c5": (1 << 19, 256, np.float64, 5, "2^22 LPs x 256 constraints fp64 sharded over 8 GPUs: 2^19 per GPU (BASELINE configs[4])"),
+}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(cfg_name):
+    """dram read+write bytes per launch from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(cfg_name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during a region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def make_batch(cfg_name, rank):
+    import paper_1902_04995_b200 as P
+
+    n, m, dt, seed, _ = CONFIGS[cfg_name]
+    sizes = np.full(n, m, np.int32)
+    pb = P.PackedBatch.generate(sizes, seed, first=rank * n)
+    return pb.astype(dt) if dt != np.float64 else pb
+
+
+def cpu_reference(pb, steps, warmup, threads=0):
+    """Time the unmodified reference solve_batch (oracle/_ref) on this host."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py as O  # test/baseline infrastructure only
+
+    ref = O.ref_lib()
+    n = pb.n
+    ax, ay, b = (np.ascontiguousarray(a, np.float64) for a in (pb.ax, pb.ay, pb.b))
+    c, M = np.ascontiguousarray(pb.c, np.float64), np.ascontiguousarray(pb.M, np.float64)
+    perm = np.ascontiguousarray(pb.perm, np.uint32)
+    off = np.ascontiguousarray(pb.offset, np.int64)
+    mm = np.ascontiguousarray(pb.m, np.int32)
+    h = ref.ref_batch_create(n, off.ctypes.data, mm.ctypes.data, ax.ctypes.data, ay.ctypes.data,
+                             b.ctypes.data, perm.ctypes.data, c.ctypes.data, M.ctypes.data)
+    fe = np.zeros(n, np.uint8); x = np.zeros(n); y = np.zeros(n); v = np.zeros(n)
+    cores = threads or os.cpu_count()
+    try:
+        for _ in range(warmup):
+            ref.ref_batch_solve(h, 512, 1, threads, 1e-12, 1e-9, None, None, None, None, None, None)
+        ns = []
+        for _ in range(steps):
+            ns.append(ref.ref_batch_solve(h, 512, 1, threads, 1e-12, 1e-9, fe.ctypes.data,
+                                          x.ctypes.data, y.ctypes.data, v.ctypes.data, None, None))
+    finally:
+        ref.ref_batch_free(h)
+    total_s = sum(ns) / 1e9
+    return {"value": n * steps / total_s, "unit": "LPs/s", "cores": cores, "kind": "reference",
+            "sample": f"{n} LPs x {int(pb.m[0])} constraints, fp64 solve_batch(balanced, width 512, "
+                      f"{cores} workers) x {steps} runs = {total_s:.2f} s wall"}
+
+
+def run_reference_arm(args, world, rank):
+    cfg = args.config
+    n, m, dt, seed, desc = CONFIGS[cfg]
+    if rank != 0:
+        return
+    pb = make_batch(cfg, 0)
+    cb = cpu_reference(pb, args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "LPs/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * n / cb["value"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "lps": n, "m": m, "parallelism": "host threads"},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "LPs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 5)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_env()
+
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1902_04995_b200 as P
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    cfg = args.config
+    n, m, dt, seed, desc = CONFIGS[cfg]
+    pb = make_batch(cfg, rank)
+    algo_bytes = pb.constraint_bytes()
+
+    # ---- device-resident kernel timing ----------------------------------------
+    db = P.DeviceBatch(pb, device=local)
+    out = db.empty_result()
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        P.solve_device(db, out, stream=stream)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for k in range(args.steps):
+            starts[k].record(stream)
+            P.solve_device(db, out, stream=stream)
+            ends[k].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    region_ms = max_over_ranks(t0.elapsed_time(t1))
+    kern_ms = float(np.mean([s.elapsed_time(e) for s, e in zip(starts, ends)]))
+    kern_ms_max = max_over_ranks(kern_ms)
+    ms_per_step = region_ms / args.steps
+    value = world * n / (ms_per_step / 1e3)
+    gpu_launches = args.steps  # one solve kernel per step
+
+    # ---- end-to-end through the C ABI with pinned host buffers ---------------
+    e2e_steps = args.e2e_steps or min(args.steps, 5)
+    pin = lambda a: _pinned_copy(torch, a)
+    hp = P.PackedBatch(pin(pb.m), pin(pb.offset), pin(pb.ax), pin(pb.ay), pin(pb.b), pin(pb.perm),
+                       pin(pb.c), pin(pb.M))
+    hout = P.PackedResult(*(pin(np.zeros(sh, d)) for sh, d in (
+        (n, np.uint8), (n, dt), (n, dt), (n, dt), ((n, 2), np.int32), (n, np.uint32), (n, np.uint64))))
+    cfgb = P.BlockConfig(workers=1)
+    P.solve_packed(hp, cfgb, out=hout)  # warm the library's device arena
+    h2d = sum(a.nbytes for a in (hp.m, hp.offset, hp.ax, hp.ay, hp.b, hp.perm, hp.c, hp.M))
+    d2h = sum(a.nbytes for a in (hout.status, hout.x, hout.y, hout.value, hout.pair,
+                                 hout.violation_events, hout.work_units))
+    barrier()
+    te0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        P.solve_packed(hp, cfgb, out=hout)
+    te1 = time.perf_counter()
+    barrier()
+    e2e_s = max_over_ranks(te1 - te0)
+    e2e_value = world * n * e2e_steps / e2e_s
+
+    # ---- rank-0 extras: parity spot check, cpu baseline, JSON line ------------
+    if rank == 0:
+        peak, peak_src = load_peaks()
+        achieved = algo_bytes / (kern_ms_max / 1e3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": "LPs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if dt == np.float32 else "f64",
+            "data": "synthetic: reference generator streams (gen_mixed, seed %d), LP j seeded by "
+                    "its global index" % seed,
+            "config": {"workload": desc, "lps_per_gpu": n, "m": m,
+                       "parallelism": "dp%d (LP-index shards, no collective)" % world,
+                       "l2": "inputs %.0f MB > 126 MB L2, no flush" % (h2d / 1e6)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": load_traffic(cfg),
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": algo_bytes,
+                         "kernel_ms": kern_ms_max},
+            "e2e": {"value": e2e_value, "unit": "LPs/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
+            "gpu_launches": gpu_launches,
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline:
+            try:
+                # ~1 s wall on all host cores (x cores = 10-30 s of CPU work)
+                line["cpu_baseline"] = cpu_reference(pb, steps=4, warmup=1)
+            except Exception as e:  # reference .so absent on this box
+                line["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _pinned_copy(torch, a):
+    t = torch.empty(a.shape, dtype=_torch_dtype(torch, a.dtype), pin_memory=True)
+    out = t.numpy().view(a.dtype)
+    out[...] = a
+    return out
+
+
+def _torch_dtype(torch, dt):
+    dt = np.dtype(dt)
+    return {np.dtype(np.uint8): torch.uint8, np.dtype(np.int32): torch.int32,
+            np.dtype(np.uint32): torch.int32, np.dtype(np.int64): torch.int64,
+            np.dtype(np.uint64): torch.int64, np.dtype(np.uint16): torch.int16,
+            np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}[dt]
+
+
+if __name__ == "__main__":
+    main()

@@ -66,8 +66,10 @@ enum { LP2D_PERM_U16 = 16, LP2D_PERM_U32 = 32 };
  *   c[2j], c[2j+1] is the objective, bound_m[j] the box half-width M.
  * Scalars are float for lp2dgpu_solve_f32 and double for lp2dgpu_solve_f64.
  * mem says whether every array is host or device memory. In device mode
- * max_m must be given (host scalar, max over m[j]); in host mode it is
- * computed when 0. */
+ * max_m must be given (host scalar, max over m[j]) and min_m should be (a
+ * lower bound; 0 if unknown): when both fall in one size class the batch is
+ * solved by a single kernel, otherwise LPs are first binned by size class on
+ * the device. In host mode both are computed. */
 typedef struct lp2d_batch_soa {
   int64_t n;
   const int32_t* m;
@@ -81,6 +83,7 @@ typedef struct lp2d_batch_soa {
   const void* c;     /* [2n] */
   const void* bound_m; /* [n] */
   int64_t max_m;
+  int64_t min_m;
 } lp2d_batch_soa;
 
 /* block_config (batch.hpp:50-58) + tolerance (core.hpp:59-68). */
@@ -122,6 +125,11 @@ int lp2dgpu_solve_f64(const lp2d_batch_soa* batch, const lp2d_opts* opts,
 /* Offsets for a batch of sizes m[0..n-1] satisfying the layout contract;
  * writes offset[0..n] and returns the total element count. */
 int64_t lp2dgpu_pack_offsets(int64_t n, const int32_t* m, int64_t* offset);
+
+/* Multi-GPU partitioner used by host mode: contiguous LP
+ * ranges [cut[g], cut[g+1]) balanced by sum(m + 4); cut has parts+1 entries.
+ * Pure host code (no CUDA). Returns 0 or LP2D_ERR_ARG. */
+int lp2dgpu_partition(int64_t n, const int32_t* m, int32_t parts, int64_t* cut);
 
 /* Device-side permutation generation (serial.hpp:138-146 shuffle with
  * rng.hpp:64-68 seeds): perm for LP j is shuffle(m[j], seeds[j]). Device

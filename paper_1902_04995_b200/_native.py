@@ -48,6 +48,7 @@ class BatchSoA(C.Structure):
         ("c", C.c_void_p),
         ("bound_m", C.c_void_p),
         ("max_m", C.c_int64),
+        ("min_m", C.c_int64),
     ]
 
 
@@ -81,6 +82,7 @@ EXPORTS = (
     "lp2dgpu_solve_f32",
     "lp2dgpu_solve_f64",
     "lp2dgpu_pack_offsets",
+    "lp2dgpu_partition",
     "lp2dgpu_shuffle_device",
     "lp2dgpu_device_count",
     "lp2dgpu_last_error",
@@ -119,6 +121,9 @@ def lib():
         fn.restype = C.c_int
     L.lp2dgpu_pack_offsets.argtypes = [C.c_int64, C.c_void_p, C.c_void_p]
     L.lp2dgpu_pack_offsets.restype = C.c_int64
+    if hasattr(L, "lp2dgpu_partition"):
+        L.lp2dgpu_partition.argtypes = [C.c_int64, C.c_void_p, C.c_int32, C.c_void_p]
+        L.lp2dgpu_partition.restype = C.c_int
     L.lp2dgpu_shuffle_device.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
     L.lp2dgpu_shuffle_device.restype = C.c_int

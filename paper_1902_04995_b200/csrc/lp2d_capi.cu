@@ -85,12 +85,6 @@ uint32_t* take_counter(int dev) {
 // Register slot classes: NS slots hold m + 4 positions (box included).
 constexpr int kSlotClasses[] = {1, 2, 3, 5, 9, 17, 33};
 
-int nslot_for(int64_t max_m) {
-  for (int ns : kSlotClasses)
-    if (max_m + 4 <= 32 * ns) return ns;
-  return -1;
-}
-
 template <typename T>
 constexpr int max_nslot() {
   return sizeof(T) == 4 ? 33 : 17;  // fp64 keeps m <= 540 in registers
@@ -105,10 +99,11 @@ double eps_hi_of(double eps_par) {
   return (double)hi;
 }
 
-template <typename T, typename P, int NSLOT>
+template <typename T, typename P, int NS, int NT = 0>
 int launch_warp_kernel(KParams kp, int dev, cudaStream_t stream) {
-  using L = WarpLayout<T, P, NSLOT>;
-  auto kern = k_solve_warp<T, P, NSLOT>;
+  using L = WarpLayout<T, P, NS, NT>;
+  constexpr int kWarpsPerCta = L::kWarps;
+  auto kern = k_solve_warp<T, P, NS, NT>;
   static int blocks_per_sm[64] = {0};
   if (!blocks_per_sm[dev]) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -129,25 +124,108 @@ int launch_warp_kernel(KParams kp, int dev, cudaStream_t stream) {
   return 0;
 }
 
+template <typename T>
+constexpr int n_reg_classes() {
+  int n = 0;
+  for (int ns : kSlotClasses)
+    if (ns <= max_nslot<T>()) ++n;
+  return n;
+}
+
+// Size class of an LP of m constraints: index into kSlotClasses, or
+// n_reg_classes<T>() for the large (global-memory) class.
+template <typename T>
+int class_of(int64_t m) {
+  for (int c = 0; c < n_reg_classes<T>(); ++c)
+    if (m + 4 <= 32 * kSlotClasses[c]) return c;
+  return n_reg_classes<T>();
+}
+
 template <typename T, typename P>
-int launch_by_slots(const KParams& kp, int nslot, int dev, cudaStream_t s) {
-  switch (nslot) {
+int launch_global_kernel(KParams kp, int dev, cudaStream_t stream) {
+  auto kern = k_solve_global<T, P>;
+  static int blocks_per_sm[64] = {0};
+  if (!blocks_per_sm[dev]) {
+    int b = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kWarpsPerCta * 32, 0));
+    blocks_per_sm[dev] = std::max(b, 1);
+  }
+  const int64_t want = (kp.n_list + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int64_t maxb = (int64_t)blocks_per_sm[dev] * g_dev[dev].sm_count;
+  const int grid = (int)std::max<int64_t>(1, std::min(want, maxb));
+  kp.total_warps = grid * kWarpsPerCta;
+  kp.counter = take_counter(dev);
+  kern<<<grid, kWarpsPerCta * 32, 0, stream>>>(kp);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <typename T, typename P>
+int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s) {
+  if (cls >= n_reg_classes<T>()) return launch_global_kernel<T, P>(kp, dev, s);
+  switch (kSlotClasses[cls]) {
     case 1: return launch_warp_kernel<T, P, 1>(kp, dev, s);
     case 2: return launch_warp_kernel<T, P, 2>(kp, dev, s);
     case 3: return launch_warp_kernel<T, P, 3>(kp, dev, s);
     case 5: return launch_warp_kernel<T, P, 5>(kp, dev, s);
     case 9: return launch_warp_kernel<T, P, 9>(kp, dev, s);
     case 17: return launch_warp_kernel<T, P, 17>(kp, dev, s);
-    case 33:
-      if constexpr (max_nslot<T>() >= 33) return launch_warp_kernel<T, P, 33>(kp, dev, s);
+    case 33:  // 17 register chunks + 16 shared-memory tail chunks
+      if constexpr (max_nslot<T>() >= 33) return launch_warp_kernel<T, P, 17, 16>(kp, dev, s);
       break;
   }
-  return fail(LP2D_ERR_UNSUPPORTED, "constraint count above the register-resident size classes");
+  return fail(LP2D_ERR_UNSUPPORTED, "size class not built");
+}
+
+// may_sync: host mode (which synchronises anyway) reads the class counts back
+// and launches only the non-empty classes with right-sized grids; device
+// mode stays asynchronous and launches every class in [min_m, max_m].
+template <typename T, typename P>
+int launch_balanced(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStream_t s,
+                    bool may_sync) {
+  const int cmin = class_of<T>(std::max<int64_t>(min_m, 0));
+  const int cmax = class_of<T>(max_m);
+  if (cmin == cmax) return launch_class<T, P>(kp, cmax, dev, s);
+  // Mixed sizes: bin LP ids by class on the device, one launch per class.
+  BinSpec spec{};
+  spec.nreg = n_reg_classes<T>();
+  for (int c = 0; c < spec.nreg; ++c) spec.slots[c] = kSlotClasses[c];
+  const size_t ws_bytes = 2 * 16 * sizeof(int32_t) + sizeof(int32_t) * (size_t)kp.n_list;
+  void* ws = nullptr;
+  CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, s));
+  int32_t* counts = static_cast<int32_t*>(ws);
+  int32_t* cursors = counts + 16;
+  int32_t* list = counts + 32;
+  CUDA_TRY(cudaMemsetAsync(counts, 0, 2 * 16 * sizeof(int32_t), s));
+  const int threads = 256;
+  const int grid = (int)std::min<int64_t>((kp.n_list + threads - 1) / threads,
+                                          (int64_t)g_dev[dev].sm_count * 8);
+  k_bin_count<<<grid, threads, 0, s>>>(kp.n_list, kp.m, spec, counts);
+  k_bin_scatter<<<grid, threads, 0, s>>>(kp.n_list, kp.m, spec, counts, cursors, list);
+  CUDA_TRY(cudaGetLastError());
+  kp.list = list;
+  kp.bin_counts = counts;
+  int32_t host_counts[16] = {0};
+  if (may_sync) {
+    CUDA_TRY(cudaMemcpyAsync(host_counts, counts, sizeof(host_counts), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  int rc = 0;
+  // Largest class first: its LPs are the longest, so they start earliest.
+  for (int c = cmax; c >= cmin && rc == 0; --c) {
+    if (may_sync && host_counts[c] == 0) continue;
+    KParams kc = kp;
+    kc.bin_class = c;
+    if (may_sync) kc.n_list = host_counts[c];
+    rc = launch_class<T, P>(kc, c, dev, s);
+  }
+  CUDA_TRY(cudaFreeAsync(ws, s));
+  return rc;
 }
 
 template <typename T>
-int launch_solve(const KParams& kp, int64_t max_m, int perm_bits, int sched, int dev,
-                 cudaStream_t s) {
+int launch_solve(const KParams& kp, int64_t min_m, int64_t max_m, int perm_bits, int sched,
+                 int dev, cudaStream_t s, bool may_sync = false) {
   if (kp.n_list == 0) return 0;
   if (sched == LP2D_SCHED_NAIVE) {
     const int threads = 128;
@@ -159,13 +237,8 @@ int launch_solve(const KParams& kp, int64_t max_m, int perm_bits, int sched, int
     CUDA_TRY(cudaGetLastError());
     return 0;
   }
-  const int nslot = nslot_for(max_m);
-  if (nslot < 0 || nslot > max_nslot<T>())
-    return fail(LP2D_ERR_UNSUPPORTED,
-                "max constraint count " + std::to_string(max_m) +
-                    " exceeds the register-resident kernel (fp32 <= 1052, fp64 <= 540)");
-  if (perm_bits == 16) return launch_by_slots<T, uint16_t>(kp, nslot, dev, s);
-  return launch_by_slots<T, uint32_t>(kp, nslot, dev, s);
+  if (perm_bits == 16) return launch_balanced<T, uint16_t>(kp, min_m, max_m, dev, s, may_sync);
+  return launch_balanced<T, uint32_t>(kp, min_m, max_m, dev, s, may_sync);
 }
 
 int validate_common(const lp2d_batch_soa* b, const lp2d_opts* o, const lp2d_out* out) {
@@ -201,7 +274,7 @@ KParams make_params(const lp2d_opts* o) {
 // ---- host mode: one shard [lo, hi) on one device ----------------------------
 template <typename T>
 int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out,
-                     int64_t lo, int64_t hi, int64_t max_m) {
+                     int64_t lo, int64_t hi, int64_t min_m, int64_t max_m) {
   if (int rc = ensure_device(dev)) return rc;
   DeviceState& d = g_dev[dev];
   std::lock_guard<std::mutex> lock(d.mu);
@@ -271,7 +344,8 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   kp.pair = reinterpret_cast<int32_t*>(A + off_pair);
   kp.viol = reinterpret_cast<uint32_t*>(A + off_viol);
   kp.wu = reinterpret_cast<uint64_t*>(A + off_wu);
-  if (int rc = launch_solve<T>(kp, max_m, b->perm_bits, o->scheduler, dev, s)) return rc;
+  if (int rc = launch_solve<T>(kp, min_m, max_m, b->perm_bits, o->scheduler, dev, s, true))
+    return rc;
   CUDA_TRY(cudaMemcpyAsync(out->status + lo, A + off_st, cnt, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(static_cast<T*>(out->x) + lo, A + off_x, sizeof(T) * cnt,
                            cudaMemcpyDeviceToHost, s));
@@ -324,11 +398,11 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
     kp.pair = out->pair;
     kp.viol = out->violation_events;
     kp.wu = out->work_units;
-    return launch_solve<T>(kp, b->max_m, b->perm_bits, o->scheduler, dev,
+    return launch_solve<T>(kp, b->min_m, b->max_m, b->perm_bits, o->scheduler, dev,
                            static_cast<cudaStream_t>(o->stream));
   }
   // host mode: validate the layout contract, then shard.
-  int64_t max_m = 0;
+  int64_t max_m = 0, min_m = INT64_MAX;
   for (int64_t j = 0; j < b->n; ++j) {
     const int64_t mj = b->m[j];
     if (mj < 0) return fail(LP2D_ERR_PERM_LENGTH, "negative constraint count");
@@ -337,32 +411,21 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
       return fail(LP2D_ERR_LAYOUT, "offset[" + std::to_string(j) +
                                        "] violates the 8-element layout contract");
     max_m = std::max(max_m, mj);
+    min_m = std::min(min_m, mj);
   }
   if (b->perm_bits == 16 && max_m > 65536)
     return fail(LP2D_ERR_ARG, "u16 permutations need m <= 65536");
   int use = o->n_gpus > 0 ? std::min(o->n_gpus, ndev) : ndev;
   use = (int)std::min<int64_t>(use, b->n);
-  // Contiguous LP ranges balanced by sum(m + 4).
   std::vector<int64_t> cut(use + 1, 0);
-  cut[use] = b->n;
-  if (use > 1) {
-    double total = 0;
-    for (int64_t j = 0; j < b->n; ++j) total += (double)b->m[j] + 4.0;
-    double acc = 0;
-    int k = 1;
-    for (int64_t j = 0; j < b->n && k < use; ++j) {
-      acc += (double)b->m[j] + 4.0;
-      while (k < use && acc >= total * k / use) cut[k++] = j + 1;
-    }
-    for (; k < use; ++k) cut[k] = b->n;
-  }
-  if (use == 1) return solve_shard_host<T>(0, b, o, out, 0, b->n, max_m);
+  lp2dgpu_partition(b->n, b->m, use, cut.data());
+  if (use == 1) return solve_shard_host<T>(0, b, o, out, 0, b->n, min_m, max_m);
   std::vector<int> rcs(use, 0);
   std::vector<std::string> errs(use);
   std::vector<std::thread> th;
   for (int g = 0; g < use; ++g) {
     th.emplace_back([&, g] {
-      if (cut[g + 1] > cut[g]) rcs[g] = solve_shard_host<T>(g, b, o, out, cut[g], cut[g + 1], max_m);
+      if (cut[g + 1] > cut[g]) rcs[g] = solve_shard_host<T>(g, b, o, out, cut[g], cut[g + 1], min_m, max_m);
       if (rcs[g]) errs[g] = g_err;
     });
   }
@@ -390,6 +453,21 @@ int lp2dgpu_solve_f32(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out
 
 int lp2dgpu_solve_f64(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
   return solve_impl<double>(b, o, out);
+}
+
+int lp2dgpu_partition(int64_t n, const int32_t* m, int32_t parts, int64_t* cut) {
+  if (n < 0 || parts < 1 || !cut || (n > 0 && !m)) return fail(LP2D_ERR_ARG, "bad partition arguments");
+  double total = 0;
+  for (int64_t j = 0; j < n; ++j) total += (double)std::max(m[j], 0) + 4.0;
+  cut[0] = 0;
+  int k = 1;
+  double acc = 0;
+  for (int64_t j = 0; j < n && k < parts; ++j) {
+    acc += (double)std::max(m[j], 0) + 4.0;
+    while (k < parts && acc >= total * k / parts) cut[k++] = j + 1;
+  }
+  for (; k <= parts; ++k) cut[k] = n;
+  return 0;
 }
 
 int64_t lp2dgpu_pack_offsets(int64_t n, const int32_t* m, int64_t* offset) {

@@ -31,6 +31,11 @@ constexpr int kWarpsPerCta = 4;
 struct KParams {
   int64_t n_list;        // LPs this launch solves
   const int32_t* list;   // LP ids (nullptr: 0..n_list-1)
+  // Size-class binning (mixed batches): when bin_counts is set, this launch
+  // solves class bin_class, i.e. the bin_counts[bin_class] ids stored in
+  // `list` after the ids of the lower classes (k_bin_* below).
+  const int32_t* bin_counts;
+  int32_t bin_class;
   const int32_t* m;
   const int64_t* offset;
   const void* ax;
@@ -69,23 +74,35 @@ __host__ __device__ constexpr uint32_t round16(uint32_t x) {
   return (x + 15u) & ~15u;
 }
 
-// Register-resident layout: NS slots of 32 lanes hold considered positions
-// P = 32*slot + lane, P in [0, m+4): positions 0..3 are the box constraints
-// (serial.hpp:47-52), P >= 4 is user constraint perm[P-4] (batch.hpp:137-139).
-// The staging buffer holds one LP of up to kCap = 32*NS-4 constraints.
-template <typename T, typename P, int NS>
+// Warp layout: considered positions P = 32*chunk + lane, P in [0, m+4);
+// positions 0..3 are the box constraints (serial.hpp:47-52), P >= 4 is user
+// constraint perm[P-4] (batch.hpp:137-139). Chunks 0..NS-1 live in REGISTERS
+// (fully unrolled, compile-time slot indices); chunks NS..NS+NT-1 (the
+// "tail", only for the largest class) live in a per-warp shared-memory copy
+// in insertion order and are walked by rolled loops, which keeps the hot code
+// under the SM's instruction cache. The staging buffer receives one LP of up
+// to kCap constraints (original order + permutation) by 1D bulk TMA.
+template <typename T, typename P, int NS, int NT>
 struct WarpLayout {
-  static constexpr int kCap = 32 * NS - 4;
+  static constexpr int kChunks = NS + NT;
+  static constexpr int kCap = 32 * kChunks - 4;
   static constexpr uint32_t kArr = round16(kCap * sizeof(T));
   static constexpr uint32_t kPerm = round16(kCap * sizeof(P));
-  static constexpr uint32_t kBuf = 3 * kArr + kPerm;  // per warp
-  static constexpr uint32_t kSmem = kWarpsPerCta * kBuf + kWarpsPerCta * 8;
-  // Occupancy target: 3 CTAs (12 warps) per SM for the big classes.
+  static constexpr uint32_t kStage = 3 * kArr + kPerm;
+  static constexpr uint32_t kTailArr = 32u * NT * sizeof(T);
+  static constexpr uint32_t kBuf = kStage + 3 * kTailArr;  // per warp
+  // Warps per CTA (4 or 5) maximising resident warps under 227 KB of smem.
+  static constexpr int blocks_for(int w) { return (int)((227u * 1024u) / (w * kBuf + w * 8u)); }
+  static constexpr int kWarps =
+      (blocks_for(5) * 5 > blocks_for(4) * 4 && blocks_for(5) >= 1) ? 5 : 4;
 #ifndef LP2D_MIN_BLOCKS
 #define LP2D_MIN_BLOCKS 3
 #endif
   static constexpr int kMinBlocks =
-      (LP2D_MIN_BLOCKS * kBuf * kWarpsPerCta <= 220 * 1024) ? LP2D_MIN_BLOCKS : 2;
+      blocks_for(kWarps) < 1 ? 1
+                             : (blocks_for(kWarps) < LP2D_MIN_BLOCKS ? blocks_for(kWarps)
+                                                                     : LP2D_MIN_BLOCKS);
+  static constexpr uint32_t kSmem = kWarps * kBuf + kWarps * 8;
 };
 
 // Per-LP header held by lane 0 between claim and solve.
@@ -98,12 +115,24 @@ struct Header {
   T cx, cy, M;
 };
 
-template <typename T, typename P, int NS>
-__device__ __forceinline__ void issue_lp(const KParams& p, int64_t j,
-                                         unsigned char* buf, uint64_t* bar,
+// This launch's LP list (see KParams::bin_counts).
+__device__ __forceinline__ void resolve_list(const KParams& p, const int32_t*& list,
+                                             int64_t& n) {
+  list = p.list;
+  n = p.n_list;
+  if (p.bin_counts) {
+    int64_t base = 0;
+    for (int c = 0; c < p.bin_class; ++c) base += p.bin_counts[c];
+    list = p.list + base;
+    n = p.bin_counts[p.bin_class];
+  }
+}
+
+template <typename L, typename T, typename P>
+__device__ __forceinline__ void issue_lp(const KParams& p, const int32_t* list,
+                                         int64_t j, unsigned char* buf, uint64_t* bar,
                                          uint64_t policy, Header<T>& h) {
-  using L = WarpLayout<T, P, NS>;
-  const int64_t lp = p.list ? (int64_t)p.list[j] : j;
+  const int64_t lp = list ? (int64_t)list[j] : j;
   const int32_t mj = p.m[lp];
   const int64_t o = p.offset[lp];
   const int64_t o1 = p.offset[lp + 1];
@@ -332,21 +361,25 @@ __device__ __noinline__ void solve_exact_global(const KParams& p, const Header<T
     }                                                                       \
     [[fallthrough]];
 
-template <typename T, typename P, int NS>
-__global__ void __launch_bounds__(kWarpsPerCta * 32,
-                                  (WarpLayout<T, P, NS>::kMinBlocks))
+template <typename T, typename P, int NS, int NT>
+__global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
+                                  (WarpLayout<T, P, NS, NT>::kMinBlocks))
     k_solve_warp(const KParams p) {
   static_assert(NS >= 1 && NS <= 40, "slot count");
-  using L = WarpLayout<T, P, NS>;
+  using L = WarpLayout<T, P, NS, NT>;
+  constexpr int W = L::kWarps;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wic = threadIdx.x >> 5;
   unsigned char* buf = smem + wic * L::kBuf;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kWarpsPerCta * L::kBuf) + wic;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + W * L::kBuf) + wic;
   const T* sax = reinterpret_cast<const T*>(buf);
   const T* say = reinterpret_cast<const T*>(buf + L::kArr);
   const T* sb = reinterpret_cast<const T*>(buf + 2 * L::kArr);
   const P* sperm = reinterpret_cast<const P*>(buf + 3 * L::kArr);
+  T* tax = reinterpret_cast<T*>(buf + L::kStage);
+  T* tay = reinterpret_cast<T*>(buf + L::kStage + L::kTailArr);
+  T* tb = reinterpret_cast<T*>(buf + L::kStage + 2 * L::kTailArr);
 
   const T eps_par = Eps<T>::par(p);
   const T eps_feas = Eps<T>::feas(p);
@@ -356,17 +389,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
   if (lane == 0) mbar_init(bar, 1);
   __syncwarp();
 
+  const int32_t* list;
+  int64_t n_list;
+  resolve_list(p, list, n_list);
   uint32_t phase = 0;
-  int64_t j = (int64_t)blockIdx.x * kWarpsPerCta + wic;
+  int64_t j = (int64_t)blockIdx.x * W + wic;
   Header<T> hn{};
-  if (lane == 0 && j < p.n_list) issue_lp<T, P, NS>(p, j, buf, bar, policy, hn);
+  if (lane == 0 && j < n_list) issue_lp<L, T, P>(p, list, j, buf, bar, policy, hn);
 
-  while (j < p.n_list) {
+  while (j < n_list) {
     const Header<T> h = bcast(hn);
     mbar_wait(bar, phase);
     phase ^= 1u;
 
-    // ---- gather: positions P = 32*K + lane in insertion order ---------------
+    // ---- gather: chunk K of the insertion order into registers / the tail --
     // Out-of-range perm entries are clamped for the load and reported through
     // pmax (status LP2D_INVALID). sbits tracks max |ax|+|ay| as float bits,
     // which orders NaN/INF above every finite value.
@@ -397,6 +433,25 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
       ray[K] = vay;
       rb[K] = vb;
     }
+    if constexpr (NT > 0) {
+#pragma unroll 1
+      for (int c = 0; c < NT; ++c) {
+        const int P_ = 32 * (NS + c) + lane;
+        T vax = T(0), vay = T(0), vb = T(INFINITY);
+        if (P_ < mpos) {
+          const uint32_t o = sperm[P_ - 4];
+          pmax = max(pmax, o);
+          const uint32_t oc = min(o, (uint32_t)(L::kCap - 1));
+          vax = sax[oc];
+          vay = say[oc];
+          vb = sb[oc];
+          sbits = max(sbits, float_bits(fabs(vax) + fabs(vay)));
+        }
+        tax[32 * c + lane] = vax;
+        tay[32 * c + lane] = vay;
+        tb[32 * c + lane] = vb;
+      }
+    }
     const bool bad = !h.ok || (mj > 0 && __reduce_max_sync(kFull, pmax) >= (uint32_t)mj);
     __syncwarp();
     fence_proxy_async_smem();
@@ -405,7 +460,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
     int64_t jn = 0;
     if (lane == 0) jn = (int64_t)atomicAdd(p.counter, 1u) + p.total_warps;
     jn = __shfl_sync(kFull, jn, 0);
-    if (lane == 0 && jn < p.n_list) issue_lp<T, P, NS>(p, jn, buf, bar, policy, hn);
+    if (lane == 0 && jn < n_list) issue_lp<L, T, P>(p, list, jn, buf, bar, policy, hn);
 
     // Per-LP parallel-test bound (see wu_fold), never below the fast
     // division's divisor floor. LPs outside the proven range go to the exact
@@ -420,11 +475,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
     lp_init(S, h);
     S.st = bad ? 255 : 0;
     const T cthr = eps_par * sqrt(h.cx * h.cx + h.cy * h.cy);
-    int s = 0;
+    int s = 0;                         // chunk where the sweep resumes
     uint32_t startmask = 0xfffffff0u;  // the box is never tested
     bool running = !bad && !wild;
     while (running) {
-      // Speculative chunked violation test from slot s onward.
+      // Speculative chunked violation test from chunk s onward.
       const T px = S.px, py = S.py;
       int sfound = -1;
       uint32_t vfound = 0;
@@ -441,10 +496,29 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
         LP2D_TEST_CASE(32) LP2D_TEST_CASE(33) LP2D_TEST_CASE(34) LP2D_TEST_CASE(35)
         LP2D_TEST_CASE(36) LP2D_TEST_CASE(37) LP2D_TEST_CASE(38) LP2D_TEST_CASE(39)
         default:
+          // The tail: chunks NS.. from shared memory, rolled.
+          if constexpr (NT > 0) {
+#pragma unroll 1
+            for (int c = (s > NS ? s : NS); c < NS + NT && 32 * c < mpos; ++c) {
+              const int q = 32 * (c - NS) + lane;
+              const T qx = tax[q], qy = tay[q], qb = tb[q];
+              const bool v = !satisfied(qx, qy, qb, px, py, eps_feas);
+              const uint32_t vm = __ballot_sync(kFull, v) & startmask;
+              startmask = kFull;
+              if (vm) {
+                hx = qx;
+                hy = qy;
+                hb = qb;
+                vfound = vm;
+                sfound = c;
+                break;
+              }
+            }
+          }
           break;
       }
       if (sfound < 0) break;
-      // Launder the slot so the work-unit loop below is one shared copy, not
+      // Launder the chunk so the work-unit loop below is one shared copy, not
       // specialised per dispatch exit.
       s = opaque_int(sfound);
 
@@ -469,6 +543,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
         const uint32_t k = 32u * K + lane;
         wu_fold(rax[K], ray[K], rb[K], l, lpbnd, k, k < pi, acc, rare);
         if (K >= s) break;
+      }
+      if constexpr (NT > 0) {
+#pragma unroll 1
+        for (int c = NS; c <= s; ++c) {
+          const int q = 32 * (c - NS) + lane;
+          const uint32_t k = 32u * c + lane;
+          wu_fold(tax[q], tay[q], tb[q], l, lpbnd, k, k < pi, acc, rare);
+        }
       }
       if (__any_sync(kFull, rare))
         acc = fold_exact_global<T, P>(p, h.off, pi, l, h.M, eps_par, eps_feas, eps_hi);
@@ -508,12 +590,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
 template <typename T, typename P>
 __global__ void __launch_bounds__(128) k_solve_naive(const KParams p) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= p.n_list) return;
+  const int32_t* list;
+  int64_t n_list;
+  resolve_list(p, list, n_list);
+  if (j >= n_list) return;
   const T eps_par = (T)p.eps_par;
   const T eps_feas = (T)p.eps_feas;
   const T eps_hi = (T)p.eps_hi;
   Header<T> h;
-  h.lp = p.list ? (int64_t)p.list[j] : j;
+  h.lp = list ? (int64_t)list[j] : j;
   h.m = p.m[h.lp];
   h.off = p.offset[h.lp];
   h.ok = h.m >= 0;
@@ -590,6 +675,108 @@ __global__ void __launch_bounds__(128) k_solve_naive(const KParams p) {
   }
   if (st == 0 && (pos0 < 4 || pos1 < 4)) st = 2;
   write_result<T, P>(p, h, st, px, py, pos0, pos1, viol, wu);
+}
+
+// Large LPs (m above the register classes) and any other LP: one warp per
+// LP straight from global memory (solve_exact_global), claimed dynamically.
+template <typename T, typename P>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_solve_global(const KParams p) {
+  const int lane = threadIdx.x & 31;
+  const int32_t* list;
+  int64_t n_list;
+  resolve_list(p, list, n_list);
+  const T eps_par = Eps<T>::par(p);
+  const T eps_feas = Eps<T>::feas(p);
+  const T eps_hi = Eps<T>::hi(p);
+  int64_t j = (int64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  while (j < n_list) {
+    Header<T> h;
+    h.lp = list ? (int64_t)list[j] : j;
+    h.m = p.m[h.lp];
+    h.off = p.offset[h.lp];
+    h.ok = h.m >= 0;
+    h.cx = static_cast<const T*>(p.c)[2 * h.lp];
+    h.cy = static_cast<const T*>(p.c)[2 * h.lp + 1];
+    h.M = static_cast<const T*>(p.bound_m)[h.lp];
+    LPState<T> S;
+    lp_init(S, h);
+    bool bad = !h.ok;
+    if (!bad) {  // validate the permutation entries
+      const P* perm = static_cast<const P*>(p.perm) + h.off;
+      uint32_t pm = 0;
+      for (int i = lane; i < h.m; i += 32) pm = max(pm, (uint32_t)perm[i]);
+      bad = h.m > 0 && __reduce_max_sync(kFull, pm) >= (uint32_t)h.m;
+    }
+    if (bad) {
+      S.st = 255;
+    } else {
+      solve_exact_global<T, P>(p, h, eps_par, eps_feas, eps_hi, S);
+    }
+    uint8_t st = S.st;
+    if (st == 0 && (S.pos0 < 4 || S.pos1 < 4)) st = 2;
+    if (lane == 0) write_result<T, P>(p, h, st, S.px, S.py, S.pos0, S.pos1, S.viol, S.wu);
+    int64_t jn = 0;
+    if (lane == 0) jn = (int64_t)atomicAdd(p.counter, 1u) + p.total_warps;
+    j = __shfl_sync(kFull, jn, 0);
+  }
+  if (lane == 0) {
+    __threadfence();
+    const uint32_t t = atomicAdd(p.counter + 1, 1u);
+    if (t == (uint32_t)p.total_warps - 1) {
+      p.counter[0] = 0;
+      p.counter[1] = 0;
+    }
+  }
+}
+
+// Size-class binning for mixed batches: class of LP j is the first register
+// class whose 32*NS slots hold m+4 positions, else the large class
+// (nclass - 1). Two passes: count, then scatter ids into class-contiguous
+// segments of `list` (order within a class is irrelevant: LPs are
+// independent).
+__device__ __forceinline__ int size_class(int32_t m, const int32_t* slots, int nreg) {
+  for (int c = 0; c < nreg; ++c)
+    if (m + 4 <= 32 * slots[c]) return c;
+  return nreg;
+}
+
+struct BinSpec {
+  int32_t slots[8];
+  int32_t nreg;
+};
+
+__global__ void k_bin_count(int64_t n, const int32_t* m, BinSpec spec, int32_t* counts) {
+  __shared__ int32_t local[9];
+  if (threadIdx.x < 9) local[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&local[size_class(m[j], spec.slots, spec.nreg)], 1);
+  __syncthreads();
+  if (threadIdx.x <= spec.nreg && local[threadIdx.x]) atomicAdd(&counts[threadIdx.x], local[threadIdx.x]);
+}
+
+__global__ void k_bin_scatter(int64_t n, const int32_t* m, BinSpec spec, const int32_t* counts,
+                              int32_t* cursors, int32_t* list) {
+  // Warp-aggregated slot reservation: one atomic per (warp, class) instead of
+  // one per LP on the same address.
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < n; j0 += stride) {
+    const int64_t j = j0 + threadIdx.x;
+    const bool in = j < n;
+    const int c = in ? size_class(m[j], spec.slots, spec.nreg) : 15;
+    const uint32_t peers = __match_any_sync(kFull, c);
+    const int leader = __ffs(peers) - 1;
+    int32_t slot = 0;
+    if (lane == leader && in) slot = atomicAdd(&cursors[c], __popc(peers));
+    slot = __shfl_sync(kFull, slot, leader) + __popc(peers & ((1u << lane) - 1u));
+    if (in) {
+      int32_t base = 0;
+      for (int q = 0; q < c; ++q) base += counts[q];
+      list[base + slot] = (int32_t)j;
+    }
+  }
 }
 
 // K1: device Fisher-Yates (serial.hpp:138-146), one thread per LP, in place.

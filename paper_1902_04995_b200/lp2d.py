@@ -356,7 +356,7 @@ def solve_packed(pb: PackedBatch, cfg: BlockConfig = BlockConfig(), tol: Toleran
                            np.zeros(pb.n, np.uint32), np.zeros(pb.n, np.uint64))
     s = N.BatchSoA(pb.n, m.ctypes.data, off.ctypes.data, ax.ctypes.data, ay.ctypes.data,
                    b.ctypes.data, perm.ctypes.data, 16 if perm.dtype == np.uint16 else 32,
-                   N.MEM_HOST, c.ctypes.data, M.ctypes.data, 0)
+                   N.MEM_HOST, c.ctypes.data, M.ctypes.data, 0, 0)
     o = _opts(cfg, tol)
     r = N.Out(out.status.ctypes.data, out.x.ctypes.data, out.y.ctypes.data, out.value.ctypes.data,
               out.pair.ctypes.data, out.violation_events.ctypes.data, out.work_units.ctypes.data)
@@ -380,6 +380,7 @@ class DeviceBatch:
         self.device = device
         self.dtype = pb.dtype
         self.max_m = int(pb.m.max(initial=0))
+        self.min_m = int(pb.m.min()) if pb.n else 0
         self.m, self.offset = t(pb.m), t(pb.offset)
         self.ax, self.ay, self.b = t(pb.ax), t(pb.ay), t(pb.b)
         self.perm = t(pb.perm.view(np.int16) if pb.perm.dtype == np.uint16 else pb.perm.view(np.int32))
@@ -410,7 +411,7 @@ def solve_device(db: DeviceBatch, out: PackedResult, cfg: BlockConfig = BlockCon
         stream = torch.cuda.current_stream(db.device)
     s = N.BatchSoA(db.n, db.m.data_ptr(), db.offset.data_ptr(), db.ax.data_ptr(), db.ay.data_ptr(),
                    db.b.data_ptr(), db.perm.data_ptr(), db.perm_bits, N.MEM_DEVICE,
-                   db.c.data_ptr(), db.M.data_ptr(), db.max_m)
+                   db.c.data_ptr(), db.M.data_ptr(), db.max_m, db.min_m)
     o = _opts(cfg, tol, device=db.device, stream=stream.cuda_stream)
     r = N.Out(out.status.data_ptr(), out.x.data_ptr(), out.y.data_ptr(), out.value.data_ptr(),
               out.pair.data_ptr() if stats else None,

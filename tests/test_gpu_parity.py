@@ -1,0 +1,241 @@
+"""Parity of the CUDA path (through the C ABI) with the reference and the
+oracle. Bit-exact everywhere: fp64 results equal the UNMODIFIED reference's
+(committed fixtures) and the fp64 oracle's; fp32 results equal the fp32
+oracle restatement's. "Equal" is IEEE value equality (== ; -0 == +0) for
+x, y, value and exact integer equality for status, defining pair,
+violation_events and work_units. The north-star tolerances (1e-5 rel fp32,
+1e-12 rel fp64) are therefore met with zero error."""
+import numpy as np
+import pytest
+
+from conftest import load_batch, load_npz
+
+pytestmark = pytest.mark.gpu
+
+SCHEDS = ("balanced", "naive")
+
+
+def _cfg(P, sched):
+    return P.BlockConfig(scheduler=getattr(P.SchedulerKind, sched))
+
+
+def assert_same_as_oracle(r, o, O, what=""):
+    st = r.status.astype(np.int32)
+    bad = np.nonzero((st != o["status"]) | (r.pair != o["pair"]).any(axis=1))[0]
+    assert bad.size == 0, f"{what}: status/pair differ at LPs {bad[:8]}"
+    feas = o["status"] != O.INFEASIBLE
+    for k in ("x", "y", "value"):
+        g = getattr(r, k)[feas].astype(np.float64)
+        assert np.array_equal(g, o[k][feas]), f"{what}: {k} differs"
+    assert np.array_equal(r.violation_events.astype(np.uint64), o["violation_events"]), what
+    assert np.array_equal(r.work_units, o["work_units"]), what
+
+
+@pytest.mark.parametrize("sched", SCHEDS)
+@pytest.mark.parametrize("name", ["c1", "mixed", "verify", "m1024"])
+def test_fp64_equals_reference_fixture(P, O, name, sched):
+    pk = load_batch(name)
+    ref = load_npz(f"ref_{name}.npz")
+    g = load_npz(f"oracle_{name}.npz")
+    r = P.solve_packed(pk.with_perm_bits(16), _cfg(P, sched))
+    feas = r.status.astype(np.int32) != O.INFEASIBLE
+    assert np.array_equal(feas, ref["feasible"].astype(bool))
+    for k in ("x", "y", "value"):
+        assert np.array_equal(getattr(r, k)[feas], ref[k][feas]), k
+    assert np.array_equal(r.violation_events.astype(np.uint64), ref["violation_events"])
+    assert np.array_equal(r.work_units, ref["work_units"])
+    assert np.array_equal(r.status.astype(np.int32), g["status64"])
+    assert np.array_equal(r.pair, g["pair64"])
+
+
+@pytest.mark.parametrize("sched", SCHEDS)
+@pytest.mark.parametrize("name", ["c1", "mixed", "verify", "m1024"])
+def test_fp32_equals_oracle_fixture(P, O, name, sched):
+    pk = load_batch(name).astype(np.float32)
+    g = load_npz(f"oracle_{name}.npz")
+    r = P.solve_packed(pk, _cfg(P, sched))
+    assert np.array_equal(r.status.astype(np.int32), g["status32"])
+    assert np.array_equal(r.pair, g["pair32"])
+    feas = g["status32"] != O.INFEASIBLE
+    for k, gk in (("x", "x32"), ("y", "y32"), ("value", "value32")):
+        assert np.array_equal(getattr(r, k)[feas].astype(np.float64), g[gk][feas]), k
+    assert np.array_equal(r.work_units, g["wu32"])
+
+
+def test_headline_config_full_size(P, O):
+    """BASELINE configs[1]: 16384 x 1024 fp32, every LP against the oracle."""
+    pb = P.PackedBatch.generate(np.full(16384, 1024, np.int32), 2).astype(np.float32)
+    r = P.solve_packed(pb)
+    assert_same_as_oracle(r, O.solve_batch(pb, threads=16), O, "c2")
+
+
+def test_orca_config_full_size(P, O):
+    """BASELINE configs[2] shape: 2^20 x 128 fp32 (one GPU's worth here)."""
+    n = 1 << 20
+    kind = np.zeros(n, np.uint8)
+    kind[::10] = 1  # every 10th LP infeasible
+    pb = P.PackedBatch.generate(np.full(n, 128, np.int32), 3, kind=kind,
+                                bscale=2e-7).astype(np.float32)
+    r = P.solve_packed(pb)
+    o = O.solve_batch(pb, threads=16)
+    assert_same_as_oracle(r, o, O, "c3")
+    assert (o["status"] == O.INFEASIBLE).sum() >= n // 10
+
+
+def test_fp64_mixed_status_config(P, O):
+    """BASELINE configs[4] shape (2^16 subset): 256 constraints fp64 with
+    10% infeasible and 10% unbounded kinds."""
+    n = 1 << 16
+    kind = np.zeros(n, np.uint8)
+    kind[3::10] = 1
+    kind[7::10] = 3
+    pb = P.PackedBatch.generate(np.full(n, 256, np.int32), 5, kind=kind)
+    r = P.solve_packed(pb)
+    o = O.solve_batch(pb, threads=16)
+    assert_same_as_oracle(r, o, O, "c5")
+    st = r.status.astype(np.int32)
+    assert (st[3::10] == O.INFEASIBLE).all() and (st[7::10] == O.UNBOUNDED).all()
+
+
+def pareto_sizes(P, seed, total):
+    L = P.lp2d.N.lib()
+    out = np.zeros(total // 8 + 1, np.int32)
+    n = L.lp2dgen_pareto_sizes(seed, 8.0, 1.0, 8192, total, len(out), out.ctypes.data)
+    return out[:n]
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_heavy_tailed_mixed_batch(P, O, dt):
+    """BASELINE configs[3] shape (2^20-constraint subset): Pareto sizes 8..8192
+    exercise every size class, the device-side binning and the large-LP
+    kernel."""
+    m = pareto_sizes(P, 4, 1 << 20)
+    pb = P.PackedBatch.generate(m, 4)
+    if dt == np.float32:
+        pb = pb.astype(np.float32)
+    r = P.solve_packed(pb)
+    assert_same_as_oracle(r, O.solve_batch(pb, threads=16), O, "c4")
+
+
+def test_large_lps_both_precisions(P, O):
+    m = np.array([1053, 2000, 541, 4100, 8192, 70000, 12], np.int32)
+    for dt in (np.float32, np.float64):
+        pb = P.PackedBatch.generate(m, 12, perm_bits=32)
+        if dt == np.float32:
+            pb = pb.astype(np.float32)
+        for sched in SCHEDS:
+            assert_same_as_oracle(P.solve_packed(pb, _cfg(P, sched)), O.solve_batch(pb), O, sched)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_size_class_edges(P, O, dt):
+    cap = 1052 if dt == np.float32 else 540
+    sizes = np.array([0, 1, 2, 3, 4, 27, 28, 29, 31, 32, 60, 61, 92, 93, 156, 157, 284, 285,
+                      540, 541 if dt == np.float32 else 539, cap], np.int32)
+    pb = P.PackedBatch.generate(np.repeat(sizes, 3), 21).astype(dt)
+    assert_same_as_oracle(P.solve_packed(pb), O.solve_batch(pb), O, "edges")
+
+
+def test_u32_permutations_and_naive(P, O):
+    pb = P.PackedBatch.generate(np.full(300, 200, np.int32), 4, perm_bits=32).astype(np.float32)
+    o = O.solve_batch(pb)
+    for sched in SCHEDS:
+        assert_same_as_oracle(P.solve_packed(pb, _cfg(P, sched)), o, O, sched)
+
+
+def test_invalid_permutation_is_flagged(P):
+    pb = P.PackedBatch.generate(np.full(8, 40, np.int32), 4)
+    pb.perm[int(pb.offset[3]) + 5] = 60000
+    r = P.solve_packed(pb)
+    assert r.status[3] == 255 and (r.status[[0, 1, 2, 4, 5, 6, 7]] != 255).all()
+
+
+def test_hand_cases_and_parallel_constraints(P, O):
+    """Axis-aligned and duplicated constraints exercise the exact parallel
+    path (test_serial.cpp:57-86 shapes)."""
+    probs = [
+        ([[1, 0, 1], [0, 1, 1]], (1, 1), 10),
+        ([[1, 0, 0], [-1, 0, -1]], (1, 1), 10),            # contradictory
+        ([[0, 1, 1], [0, 1, 1], [0, 2, 2], [1, 0, 2]], (1, 1), 10),  # parallel/duplicate
+        ([[0, 1, 1], [0, -1, -2]], (0, 1), 10),            # parallel infeasible
+        ([[1, 1, 2], [1, -1, 0], [-1, 0, 0]], (0, 1), 10),  # ties
+        ([], (-1, -1), 5),
+    ]
+    batch = P.Batch([P.Problem(c, np.array(cons, float).reshape(-1, 3), M) for cons, c, M in probs],
+                    [P.identity_permutation(len(cons)) for cons, _, _ in probs])
+    for dt in (np.float64, np.float32):
+        pb = P.PackedBatch.from_batch(batch, dtype=dt)
+        for sched in SCHEDS:
+            assert_same_as_oracle(P.solve_packed(pb, _cfg(P, sched)), O.solve_batch(pb), O, sched)
+
+
+def test_wild_magnitudes_take_the_exact_path(P, O):
+    rng = np.random.default_rng(5)
+    pb = P.PackedBatch.generate(np.full(64, 50, np.int32), 8).astype(np.float32)
+    pb.ax[: int(pb.offset[8])] *= np.float32(1e20)  # |a| >= 2^61: exact path
+    pb.b[int(pb.offset[16]):int(pb.offset[24])] *= np.float32(1e-30)
+    pb.ay[int(pb.offset[30]):int(pb.offset[31])] = 0.0
+    assert_same_as_oracle(P.solve_packed(pb), O.solve_batch(pb), O, "wild")
+
+
+def test_batch_api_matches_serial_semantics(P, O):
+    """test_batch.cpp:55-74: both schedulers == serial, stats equal."""
+    base = P.gen(128, 77)
+    b = P.replicate(base, 96, 5)
+    pb = P.PackedBatch.from_batch(b)
+    o = O.solve_batch(pb)
+    for sched in SCHEDS:
+        res = P.solve_batch(b, _cfg(P, sched))
+        assert res.stats.violation_events == int(o["violation_events"].sum())
+        assert res.stats.total_wu == int(o["work_units"].sum())
+        for j, s in enumerate(res.solutions):
+            assert s.feasible == (o["status"][j] != O.INFEASIBLE)
+            assert s.point == (o["x"][j], o["y"][j]) and s.value == o["value"][j]
+
+
+def test_device_mode_matches_host_mode(P):
+    import torch
+
+    pb = P.PackedBatch.generate(np.full(2048, 300, np.int32), 6).astype(np.float32)
+    host = P.solve_packed(pb)
+    db = P.DeviceBatch(pb)
+    out = db.empty_result()
+    P.solve_device(db, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.status.cpu().numpy(), host.status)
+    assert np.array_equal(out.x.cpu().numpy(), host.x)
+    assert np.array_equal(out.pair.cpu().numpy(), host.pair)
+    # repeated launches reuse the self-resetting ticket counters
+    for _ in range(5):
+        P.solve_device(db, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.value.cpu().numpy(), host.value)
+
+
+def test_device_shuffle_matches_host(P):
+    import ctypes as C
+
+    import torch
+
+    m = np.array([1, 2, 10, 16, 1000, 4096], np.int32)
+    off = P.lp2d.pack_offsets(m)
+    seeds = np.array([P.derive_seed(7, j) for j in range(len(m))], np.uint64)
+    dev = torch.device("cuda", 0)
+    for bits, tdt in ((16, torch.int16), (32, torch.int32)):
+        perm = torch.zeros(int(off[-1]), dtype=tdt, device=dev)
+        dm, doff = torch.from_numpy(m).to(dev), torch.from_numpy(off).to(dev)
+        ds = torch.from_numpy(seeds.view(np.int64)).to(dev)
+        rc = P.lp2d.N.lib().lp2dgpu_shuffle_device(len(m), dm.data_ptr(), doff.data_ptr(), ds.data_ptr(),
+                                                    perm.data_ptr(), bits, 0, None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        got = perm.cpu().numpy().view(np.uint16 if bits == 16 else np.uint32)
+        for j in range(len(m)):
+            o = int(off[j])
+            assert np.array_equal(got[o:o + m[j]], P.shuffle(int(m[j]), int(seeds[j])).order)
+
+
+def test_smoke_entry_point():
+    import __graft_entry__
+
+    __graft_entry__.smoke()
