@@ -309,7 +309,7 @@ def main():
         if not args.no_cpu_baseline:
             try:
                 # ~1 s wall on all host cores (x cores = 10-30 s of CPU work)
-                line["cpu_baseline"] = cpu_reference(pb, steps=4, warmup=1)
+                line["cpu_baseline"] = cpu_reference(pb, steps=8, warmup=1)
             except Exception as e:  # reference .so absent on this box
                 line["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
         print(json.dumps(line), flush=True)

@@ -27,6 +27,10 @@
 namespace lp2d_b200 {
 
 constexpr int kWarpsPerCta = 4;
+#ifndef LP2D_WU_GROUP
+#define LP2D_WU_GROUP 2
+#endif
+constexpr int kWuGroup = LP2D_WU_GROUP;
 
 struct KParams {
   int64_t n_list;        // LPs this launch solves
@@ -413,21 +417,23 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
     decltype(float_bits(T(0))) sbits = 0;
 #pragma unroll
     for (int K = 0; K < NS; ++K) {
+      // Branch-free so the loads of consecutive chunks overlap: every lane
+      // loads (clamped, always in bounds) and padding is selected after.
       const int P_ = 32 * K + lane;
+      const bool valid = P_ < mpos && !(K == 0 && P_ < 4);
+      const uint32_t o_raw = sperm[K == 0 ? max(P_ - 4, 0) : P_ - 4];
+      const uint32_t o = valid ? o_raw : 0u;
+      pmax = max(pmax, o);
+      const uint32_t oc = min(o, (uint32_t)(L::kCap - 1));
       // padding positions (>= m+4) never violate: 0*px + 0*py <= +INF
-      T vax = T(0), vay = T(0), vb = T(INFINITY);
+      T vax = valid ? sax[oc] : T(0);
+      T vay = valid ? say[oc] : T(0);
+      T vb = valid ? sb[oc] : T(INFINITY);
+      sbits = max(sbits, float_bits(fabs(vax) + fabs(vay)));
       if (K == 0 && P_ < 4) {
         vax = P_ == 0 ? T(1) : (P_ == 1 ? T(-1) : T(0));
         vay = P_ == 2 ? T(1) : (P_ == 3 ? T(-1) : T(0));
         vb = h.M;
-      } else if (P_ < mpos) {
-        const uint32_t o = sperm[P_ - 4];
-        pmax = max(pmax, o);
-        const uint32_t oc = min(o, (uint32_t)(L::kCap - 1));
-        vax = sax[oc];
-        vay = say[oc];
-        vb = sb[oc];
-        sbits = max(sbits, float_bits(fabs(vax) + fabs(vay)));
       }
       rax[K] = vax;
       ray[K] = vay;
@@ -538,18 +544,22 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
       acc.uR = T(INFINITY);
       acc.oL = acc.oR = acc.par = kNone;
       bool rare = false;
+      // Chunks are folded in pairs between exit checks, so the division
+      // chains of a pair overlap (a chunk past s is fully masked).
 #pragma unroll
       for (int K = 0; K < NS; ++K) {
         const uint32_t k = 32u * K + lane;
         wu_fold(rax[K], ray[K], rb[K], l, lpbnd, k, k < pi, acc, rare);
-        if (K >= s) break;
+        if ((K % kWuGroup == kWuGroup - 1) && K >= s) break;
       }
       if constexpr (NT > 0) {
 #pragma unroll 1
-        for (int c = NS; c <= s; ++c) {
+        for (int c = NS; c <= s; c += 2) {
           const int q = 32 * (c - NS) + lane;
           const uint32_t k = 32u * c + lane;
           wu_fold(tax[q], tay[q], tb[q], l, lpbnd, k, k < pi, acc, rare);
+          if (c + 1 < NS + NT)
+            wu_fold(tax[q + 32], tay[q + 32], tb[q + 32], l, lpbnd, k + 32, k + 32 < pi, acc, rare);
         }
       }
       if (__any_sync(kFull, rare))

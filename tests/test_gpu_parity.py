@@ -239,3 +239,18 @@ def test_smoke_entry_point():
     import __graft_entry__
 
     __graft_entry__.smoke()
+
+
+def test_cpp_drop_in_against_reference_headers():
+    """tests/cpp/shim_test.cpp: the reference's own types and solver, compiled
+    with include/lp2d_b200/solve_batch.hpp (built where /root/reference is)."""
+    import os
+    import subprocess
+
+    from conftest import ROOT
+
+    exe = os.path.join(ROOT, "tests", "cpp", "build", "shim_test")
+    if not os.path.exists(exe):
+        pytest.skip("shim_test not built (needs the reference headers)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
