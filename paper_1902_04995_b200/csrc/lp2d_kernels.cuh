@@ -93,8 +93,12 @@ struct WarpLayout {
   static constexpr uint32_t kArr = round16(kCap * sizeof(T));
   static constexpr uint32_t kPerm = round16(kCap * sizeof(P));
   static constexpr uint32_t kStage = 3 * kArr + kPerm;
-  static constexpr uint32_t kTailArr = 32u * NT * sizeof(T);
-  static constexpr uint32_t kBuf = kStage + 3 * kTailArr;  // per warp
+  // The tail is read in place from the staging buffer (through the
+  // permutation), so the buffer lives until the LP is solved and the next
+  // LP's TMA is issued at the end of the solve instead of the start. That
+  // keeps the big class at 14.7 KB of shared memory per warp (15 warps/SM).
+  static constexpr bool kLateTma = NT > 0;
+  static constexpr uint32_t kBuf = kStage;  // per warp
   // Warps per CTA (4 or 5) maximising resident warps under 227 KB of smem.
   static constexpr int blocks_for(int w) { return (int)((227u * 1024u) / (w * kBuf + w * 8u)); }
   static constexpr int kWarps =
@@ -163,6 +167,75 @@ __device__ __forceinline__ void issue_lp(const KParams& p, const int32_t* list,
   h.M = static_cast<const T*>(p.bound_m)[lp];
 }
 
+// Lane-distributed LP header: lane f < 7 holds field f of one LP's header
+// in a single 64-bit register (0 lp, 1 m, 2 offset[lp], 3 offset[lp+1],
+// 4 cx, 5 cy, 6 M as raw bits). Seven loads in flight for the price of one
+// register per lane, so a whole header can ride a pipeline stage.
+template <typename T>
+__device__ __forceinline__ uint64_t to_bits64(T v) {
+  if constexpr (sizeof(T) == 4) return (uint64_t)__float_as_uint(v);
+  else return (uint64_t)__double_as_longlong(v);
+}
+template <typename T>
+__device__ __forceinline__ T from_bits64(uint64_t u) {
+  if constexpr (sizeof(T) == 4) return __uint_as_float((uint32_t)u);
+  else return __longlong_as_double((long long)u);
+}
+
+// All lanes call; lp must be warp-uniform (lp < 0: no LP).
+template <typename T>
+__device__ __forceinline__ uint64_t load_header_field(const KParams& p, int64_t lp, int lane) {
+  if (lane == 0) return (uint64_t)lp;  // -1 (no LP) propagates
+  if (lp < 0 || lane > 6) return 0;
+  const T* c = static_cast<const T*>(p.c);
+  switch (lane) {
+    case 1: return (uint64_t)(uint32_t)p.m[lp];
+    case 2: return (uint64_t)p.offset[lp];
+    case 3: return (uint64_t)p.offset[lp + 1];
+    case 4: return to_bits64(c[2 * lp]);
+    case 5: return to_bits64(c[2 * lp + 1]);
+    default: return to_bits64(static_cast<const T*>(p.bound_m)[lp]);
+  }
+}
+
+template <typename L, typename T>
+__device__ __forceinline__ Header<T> unpack_header(uint64_t f) {
+  Header<T> h;
+  h.lp = (int64_t)__shfl_sync(kFull, f, 0);
+  h.m = (int32_t)(uint32_t)__shfl_sync(kFull, f, 1);
+  h.off = (int64_t)__shfl_sync(kFull, f, 2);
+  const int64_t o1 = (int64_t)__shfl_sync(kFull, f, 3);
+  h.cx = from_bits64<T>(__shfl_sync(kFull, f, 4));
+  h.cy = from_bits64<T>(__shfl_sync(kFull, f, 5));
+  h.M = from_bits64<T>(__shfl_sync(kFull, f, 6));
+  const int64_t cap8 = ((int64_t)h.m + 7) & ~int64_t(7);
+  h.ok = h.m >= 0 && h.m <= L::kCap && (h.off & 7) == 0 && o1 - h.off >= cap8;
+  return h;
+}
+
+// Lane 0: stage an LP's ax/ay/b/perm segments into the warp's buffer with
+// 1D bulk copies completing on the warp's mbarrier (no bytes if !ok).
+template <typename L, typename T, typename P>
+__device__ __forceinline__ void issue_tma(const KParams& p, const Header<T>& h,
+                                          unsigned char* buf, uint64_t* bar, uint64_t policy) {
+  const uint32_t bt = h.ok ? round16((uint32_t)h.m * sizeof(T)) : 0u;
+  const uint32_t bp = h.ok ? round16((uint32_t)h.m * sizeof(P)) : 0u;
+  mbar_arrive_expect_tx(bar, 3 * bt + bp);
+  if (bt) {
+    bulk_g2s(buf, static_cast<const T*>(p.ax) + h.off, bt, bar, policy);
+    bulk_g2s(buf + L::kArr, static_cast<const T*>(p.ay) + h.off, bt, bar, policy);
+    bulk_g2s(buf + 2 * L::kArr, static_cast<const T*>(p.b) + h.off, bt, bar, policy);
+    bulk_g2s(buf + 3 * L::kArr, static_cast<const P*>(p.perm) + h.off, bp, bar, policy);
+  }
+}
+
+// Defining-pair export: box k -> -(k+1), user position 4+i -> perm[i].
+__device__ __forceinline__ int32_t pair_code(uint32_t pos, uint32_t orig) {
+  if (pos == kNone) return (int32_t)0x80000000;
+  if (pos < 4) return -(int32_t)pos - 1;
+  return (int32_t)orig;
+}
+
 template <typename T>
 __device__ __forceinline__ Header<T> bcast(const Header<T>& h) {
   Header<T> r;
@@ -174,6 +247,24 @@ __device__ __forceinline__ Header<T> bcast(const Header<T>& h) {
   r.cy = __shfl_sync(kFull, h.cy, 0);
   r.M = __shfl_sync(kFull, h.M, 0);
   return r;
+}
+
+template <typename T>
+__device__ __forceinline__ void write_main(const KParams& p, const Header<T>& h, uint8_t st,
+                                           T px, T py, uint32_t viol, uint64_t wu) {
+  const int64_t lp = h.lp;
+  p.status[lp] = st;
+  T vx = T(0), vy = T(0), vv = T(0);
+  if (st == 0 || st == 2) {
+    vx = px;
+    vy = py;
+    vv = h.cx * px + h.cy * py;  // serial.hpp:187 objective_value
+  }
+  static_cast<T*>(p.x)[lp] = vx;
+  static_cast<T*>(p.y)[lp] = vy;
+  static_cast<T*>(p.value)[lp] = vv;
+  if (p.viol) p.viol[lp] = viol;
+  if (p.wu) p.wu[lp] = wu;
 }
 
 template <typename T, typename P>
@@ -265,41 +356,61 @@ __device__ __forceinline__ void lp_init(LPState<T>& S, const Header<T>& h) {
   S.st = 0;
 }
 
-// Merge the lanes' folded intervals and resolve the 1D program on l
-// (serial.hpp:95-111), for the violation at considered position pi. Returns
-// false when the LP turned out infeasible (S.st = 1).
+// Lanes' folded intervals merged over the warp (order-independent exact
+// min/max, serial.hpp:60-63; owners tie to the smallest position).
+template <typename T>
+struct Merged {
+  T uL, uR;
+  uint32_t oL, oR, par;
+};
+
+template <typename T>
+__device__ __forceinline__ Merged<T> merge_lanes(const Acc<T>& acc, bool with_par) {
+  Merged<T> mg;
+  T nuR;
+  // The reductions are independent: issued back to back, no branch between.
+  warp_best(acc.uL, acc.oL, mg.uL, mg.oL);
+  warp_best(-acc.uR, acc.oR, nuR, mg.oR);
+  mg.uR = -nuR;
+  mg.par = with_par ? __reduce_min_sync(kFull, acc.par) : kNone;
+  return mg;
+}
+
+// Resolve the 1D program on l (serial.hpp:95-111) for the violation at
+// considered position pi. Returns false when the LP turned out infeasible.
+template <typename T>
+__device__ __forceinline__ bool resolve_merged(LPState<T>& S, const Merged<T>& mg,
+                                               const Line<T>& l, uint32_t pi,
+                                               const Header<T>& h, T cthr, T eps_feas) {
+  if (mg.par != kNone) {  // serial.hpp:97 parallel-infeasible
+    S.st = 1;
+    S.pos0 = pi;
+    S.pos1 = mg.par;
+    return false;
+  }
+  const T scale = fmax(fabs(mg.uL), fabs(mg.uR));
+  if (mg.uL > mg.uR + feas_slack(eps_feas, scale)) {  // serial.hpp:98-101
+    S.st = 1;
+    S.pos0 = pi;
+    S.pos1 = mg.oL;
+    return false;
+  }
+  const T along = h.cx * l.dx + h.cy * l.dy;  // serial.hpp:102-108
+  const bool take_right = !(fabs(along) <= cthr) && along > T(0);
+  const T t = take_right ? mg.uR : mg.uL;
+  S.px = l.ox + t * l.dx;
+  S.py = l.oy + t * l.dy;
+  S.pos0 = pi;
+  S.pos1 = take_right ? mg.oR : mg.oL;
+  return true;
+}
+
 template <typename T>
 __device__ __forceinline__ bool resolve_event(LPState<T>& S, const Acc<T>& acc,
                                               const Line<T>& l, uint32_t pi,
                                               const Header<T>& h, T cthr,
                                               T eps_feas) {
-  const uint32_t par = __reduce_min_sync(kFull, acc.par);
-  if (par != kNone) {  // serial.hpp:97 parallel-infeasible
-    S.st = 1;
-    S.pos0 = pi;
-    S.pos1 = par;
-    return false;
-  }
-  T uL, nuR;
-  uint32_t oL, oR;
-  warp_best(acc.uL, acc.oL, uL, oL);
-  warp_best(-acc.uR, acc.oR, nuR, oR);
-  const T uR = -nuR;
-  const T scale = fmax(fabs(uL), fabs(uR));
-  if (uL > uR + feas_slack(eps_feas, scale)) {  // serial.hpp:98-101
-    S.st = 1;
-    S.pos0 = pi;
-    S.pos1 = oL;
-    return false;
-  }
-  const T along = h.cx * l.dx + h.cy * l.dy;  // serial.hpp:102-108
-  const bool take_right = !(fabs(along) <= cthr) && along > T(0);
-  const T t = take_right ? uR : uL;
-  S.px = l.ox + t * l.dx;
-  S.py = l.oy + t * l.dy;
-  S.pos0 = pi;
-  S.pos1 = take_right ? oR : oL;
-  return true;
+  return resolve_merged(S, merge_lanes(acc, true), l, pi, h, cthr, eps_feas);
 }
 
 // Whole-LP exact solve straight from global memory (no register staging):
@@ -381,9 +492,14 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
   const T* say = reinterpret_cast<const T*>(buf + L::kArr);
   const T* sb = reinterpret_cast<const T*>(buf + 2 * L::kArr);
   const P* sperm = reinterpret_cast<const P*>(buf + 3 * L::kArr);
-  T* tax = reinterpret_cast<T*>(buf + L::kStage);
-  T* tay = reinterpret_cast<T*>(buf + L::kStage + L::kTailArr);
-  T* tb = reinterpret_cast<T*>(buf + L::kStage + 2 * L::kTailArr);
+  // tail chunk c, lane -> the staged constraint behind position 32*(NS+c)+lane
+  auto tail_load = [&](int c, T& x, T& y, T& bb) {
+    const int P_ = 32 * (NS + c) + lane;
+    const uint32_t o = min((uint32_t)sperm[min(P_ - 4, L::kCap - 1)], (uint32_t)(L::kCap - 1));
+    x = sax[o];
+    y = say[o];
+    bb = sb[o];
+  };
 
   const T eps_par = Eps<T>::par(p);
   const T eps_feas = Eps<T>::feas(p);
@@ -397,12 +513,25 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
   int64_t n_list;
   resolve_list(p, list, n_list);
   uint32_t phase = 0;
-  int64_t j = (int64_t)blockIdx.x * W + wic;
-  Header<T> hn{};
-  if (lane == 0 && j < n_list) issue_lp<L, T, P>(p, list, j, buf, bar, policy, hn);
+  // Software pipeline per warp, one stage per solved LP so no long-latency
+  // result is consumed in the iteration that requested it:
+  //   ticket (atomic, lane 0) -> header fields (lane-distributed loads)
+  //   -> TMA of the segments -> gather + solve.
+  // The first two LPs of a warp are static (warp id, warp id + #warps).
+  const int64_t TW = p.total_warps;
+  const int64_t j0 = (int64_t)blockIdx.x * W + wic;
+  auto lp_of = [&](int64_t t) -> int64_t { return t < n_list ? (list ? (int64_t)list[t] : t) : -1; };
+  uint64_t hA = load_header_field<T>(p, lp_of(j0), lane);       // LP being solved
+  uint64_t hB = load_header_field<T>(p, lp_of(j0 + TW), lane);  // LP being staged
+  int64_t ticket = 0;
+  if (lane == 0) ticket = (int64_t)atomicAdd(p.counter, 1u) + 2 * TW;
+  Header<T> h = unpack_header<L, T>(hA);
+  if (lane == 0 && h.lp >= 0) issue_tma<L, T, P>(p, h, buf, bar, policy);
+  // deferred pair export of the previous LP (lanes 0 and 1)
+  int64_t pend_lp = -1;
+  uint32_t pend_pos = kNone, pend_q = 0;
 
-  while (j < n_list) {
-    const Header<T> h = bcast(hn);
+  while (h.lp >= 0) {
     mbar_wait(bar, phase);
     phase ^= 1u;
 
@@ -439,34 +568,30 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
       ray[K] = vay;
       rb[K] = vb;
     }
-    if constexpr (NT > 0) {
+    if constexpr (NT > 0) {  // tail: validate and bound only (read in place later)
 #pragma unroll 1
-      for (int c = 0; c < NT; ++c) {
+      for (int c = 0; c < NT && 32 * (NS + c) < mpos; ++c) {
         const int P_ = 32 * (NS + c) + lane;
-        T vax = T(0), vay = T(0), vb = T(INFINITY);
         if (P_ < mpos) {
           const uint32_t o = sperm[P_ - 4];
           pmax = max(pmax, o);
           const uint32_t oc = min(o, (uint32_t)(L::kCap - 1));
-          vax = sax[oc];
-          vay = say[oc];
-          vb = sb[oc];
-          sbits = max(sbits, float_bits(fabs(vax) + fabs(vay)));
+          sbits = max(sbits, float_bits(fabs(sax[oc]) + fabs(say[oc])));
         }
-        tax[32 * c + lane] = vax;
-        tay[32 * c + lane] = vay;
-        tb[32 * c + lane] = vb;
       }
     }
     const bool bad = !h.ok || (mj > 0 && __reduce_max_sync(kFull, pmax) >= (uint32_t)mj);
     __syncwarp();
     fence_proxy_async_smem();
 
-    // ---- claim + prefetch the next LP (overlaps this LP's solve) ------------
-    int64_t jn = 0;
-    if (lane == 0) jn = (int64_t)atomicAdd(p.counter, 1u) + p.total_warps;
-    jn = __shfl_sync(kFull, jn, 0);
-    if (lane == 0 && jn < n_list) issue_lp<L, T, P>(p, list, jn, buf, bar, policy, hn);
+    // ---- advance the pipeline (all inputs were requested an LP ago) --------
+    const Header<T> hn = unpack_header<L, T>(hB);
+    if constexpr (!L::kLateTma)
+      if (lane == 0 && hn.lp >= 0) issue_tma<L, T, P>(p, hn, buf, bar, policy);
+    const int64_t tk = __shfl_sync(kFull, ticket, 0);
+    hB = load_header_field<T>(p, lp_of(tk), lane);
+    if (lane == 0) ticket = (int64_t)atomicAdd(p.counter, 1u) + 2 * TW;
+    if (pend_lp >= 0 && lane < 2 && p.pair) p.pair[2 * pend_lp + lane] = pair_code(pend_pos, pend_q);
 
     // Per-LP parallel-test bound (see wu_fold), never below the fast
     // division's divisor floor. LPs outside the proven range go to the exact
@@ -506,9 +631,9 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
           if constexpr (NT > 0) {
 #pragma unroll 1
             for (int c = (s > NS ? s : NS); c < NS + NT && 32 * c < mpos; ++c) {
-              const int q = 32 * (c - NS) + lane;
-              const T qx = tax[q], qy = tay[q], qb = tb[q];
-              const bool v = !satisfied(qx, qy, qb, px, py, eps_feas);
+              T qx, qy, qb;
+              tail_load(c - NS, qx, qy, qb);
+              const bool v = (32 * c + lane < mpos) && !satisfied(qx, qy, qb, px, py, eps_feas);
               const uint32_t vm = __ballot_sync(kFull, v) & startmask;
               startmask = kFull;
               if (vm) {
@@ -544,27 +669,34 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
       acc.uR = T(INFINITY);
       acc.oL = acc.oR = acc.par = kNone;
       bool rare = false;
+      const int rel = (int)pi - lane;  // position 32*K + lane < pi  <=>  32*K < rel
       // Chunks are folded in pairs between exit checks, so the division
-      // chains of a pair overlap (a chunk past s is fully masked).
+      // chains of a pair overlap (a chunk past s is fully masked). Owners are
+      // recorded as chunk indices (immediates) and turned into positions after.
 #pragma unroll
       for (int K = 0; K < NS; ++K) {
-        const uint32_t k = 32u * K + lane;
-        wu_fold(rax[K], ray[K], rb[K], l, lpbnd, k, k < pi, acc, rare);
+        wu_fold(rax[K], ray[K], rb[K], l, lpbnd, (uint32_t)K, 32 * K < rel, acc, rare);
         if ((K % kWuGroup == kWuGroup - 1) && K >= s) break;
       }
       if constexpr (NT > 0) {
 #pragma unroll 1
         for (int c = NS; c <= s; c += 2) {
-          const int q = 32 * (c - NS) + lane;
-          const uint32_t k = 32u * c + lane;
-          wu_fold(tax[q], tay[q], tb[q], l, lpbnd, k, k < pi, acc, rare);
-          if (c + 1 < NS + NT)
-            wu_fold(tax[q + 32], tay[q + 32], tb[q + 32], l, lpbnd, k + 32, k + 32 < pi, acc, rare);
+          T x0, y0, b0, x1, y1, b1;
+          tail_load(c - NS, x0, y0, b0);
+          tail_load(min(c + 1, NS + NT - 1) - NS, x1, y1, b1);
+          wu_fold(x0, y0, b0, l, lpbnd, (uint32_t)c, 32 * c < rel, acc, rare);
+          wu_fold(x1, y1, b1, l, lpbnd, (uint32_t)(c + 1), 32 * (c + 1) < rel, acc, rare);
         }
       }
-      if (__any_sync(kFull, rare))
+      acc.oL = acc.oL == kNone ? kNone : ((acc.oL << 5) | (uint32_t)lane);
+      acc.oR = acc.oR == kNone ? kNone : ((acc.oR << 5) | (uint32_t)lane);
+      const bool rare_any = __any_sync(kFull, rare);
+      Merged<T> mg = merge_lanes(acc, false);
+      if (rare_any) {
         acc = fold_exact_global<T, P>(p, h.off, pi, l, h.M, eps_par, eps_feas, eps_hi);
-      if (!resolve_event(S, acc, l, pi, h, cthr, eps_feas)) break;
+        mg = merge_lanes(acc, true);
+      }
+      if (!resolve_merged(S, mg, l, pi, h, cthr, eps_feas)) break;
       if (!(fabs(S.px) < T(INFINITY) && fabs(S.py) < T(INFINITY))) {
         wild = true;  // the padding test needs a finite optimum
         break;
@@ -577,11 +709,24 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
       }
     }
     if (wild && !bad) solve_exact_global<T, P>(p, h, eps_par, eps_feas, eps_hi, S);
+    if constexpr (L::kLateTma) {  // the tail lived in the staging buffer until now
+      __syncwarp();
+      fence_proxy_async_smem();
+      if (lane == 0 && hn.lp >= 0) issue_tma<L, T, P>(p, hn, buf, bar, policy);
+    }
     uint8_t st = S.st;
     if (st == 0 && (S.pos0 < 4 || S.pos1 < 4)) st = 2;
-    if (lane == 0) write_result<T, P>(p, h, st, S.px, S.py, S.pos0, S.pos1, S.viol, S.wu);
-    j = jn;
+    if (lane == 0) write_main(p, h, st, S.px, S.py, S.viol, S.wu);
+    // pair export: lanes 0/1 request perm[pos-4] now, store one LP later
+    pend_lp = h.lp;
+    pend_pos = lane == 0 ? S.pos0 : S.pos1;
+    if (st == 255) pend_pos = kNone;
+    pend_q = 0;
+    if (lane < 2 && pend_pos != kNone && pend_pos >= 4)
+      pend_q = static_cast<const P*>(p.perm)[h.off + pend_pos - 4];
+    h = hn;
   }
+  if (pend_lp >= 0 && lane < 2 && p.pair) p.pair[2 * pend_lp + lane] = pair_code(pend_pos, pend_q);
 
   // Self-reset of the ticket counter by the last warp to finish, so the next
   // launch on this counter slot starts from zero without a memset.
