@@ -22,6 +22,8 @@
 // (PAPER.md "RGB Naive"; batch.hpp:241-256).
 #pragma once
 
+#include <type_traits>
+
 #include "lp2d_device.cuh"
 
 namespace lp2d_b200 {
@@ -167,47 +169,84 @@ __device__ __forceinline__ void issue_lp(const KParams& p, const int32_t* list,
   h.M = static_cast<const T*>(p.bound_m)[lp];
 }
 
-// Lane-distributed LP header: lane f < 7 holds field f of one LP's header
-// in a single 64-bit register (0 lp, 1 m, 2 offset[lp], 3 offset[lp+1],
-// 4 cx, 5 cy, 6 M as raw bits). Seven loads in flight for the price of one
-// register per lane, so a whole header can ride a pipeline stage.
-template <typename T>
-__device__ __forceinline__ uint64_t to_bits64(T v) {
-  if constexpr (sizeof(T) == 4) return (uint64_t)__float_as_uint(v);
-  else return (uint64_t)__double_as_longlong(v);
+// Predicated loads / atomics in inline PTX: issued exactly where written and
+// never merged through a branch, so a pipeline stage's request does not make
+// the warp wait for its result (the consumer is one LP later).
+__device__ __forceinline__ uint32_t ldg_u32_if(const void* addr, bool pred) {
+  uint32_t v = 0;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
+      : "+r"(v)
+      : "l"(addr), "r"((uint32_t)pred)
+      : "memory");
+  return v;
 }
-template <typename T>
-__device__ __forceinline__ T from_bits64(uint64_t u) {
-  if constexpr (sizeof(T) == 4) return __uint_as_float((uint32_t)u);
-  else return __longlong_as_double((long long)u);
+__device__ __forceinline__ uint32_t ldg_u16_if(const void* addr, bool pred) {
+  uint32_t v = 0;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t.reg .u16 t;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+      "@q ld.global.nc.u16 t, [%1];\n\t@q cvt.u32.u16 %0, t;\n\t}"
+      : "+r"(v)
+      : "l"(addr), "r"((uint32_t)pred)
+      : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t atomic_add_if(uint32_t* addr, bool pred) {
+  uint32_t v = 0;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q atom.global.add.u32 %0, [%1], 1;\n\t}"
+      : "+r"(v)
+      : "l"(addr), "r"((uint32_t)pred)
+      : "memory");
+  return v;
 }
 
-// All lanes call; lp must be warp-uniform (lp < 0: no LP).
+// Lane-distributed LP header: lane w holds 32-bit word w of one LP's header
+// (0 m; 1,2 offset[lp]; 3,4 offset[lp+1]; then cx, cy, M as raw words), one
+// register per lane, all words requested by a single predicated load.
 template <typename T>
-__device__ __forceinline__ uint64_t load_header_field(const KParams& p, int64_t lp, int lane) {
-  if (lane == 0) return (uint64_t)lp;  // -1 (no LP) propagates
-  if (lp < 0 || lane > 6) return 0;
-  const T* c = static_cast<const T*>(p.c);
-  switch (lane) {
-    case 1: return (uint64_t)(uint32_t)p.m[lp];
-    case 2: return (uint64_t)p.offset[lp];
-    case 3: return (uint64_t)p.offset[lp + 1];
-    case 4: return to_bits64(c[2 * lp]);
-    case 5: return to_bits64(c[2 * lp + 1]);
-    default: return to_bits64(static_cast<const T*>(p.bound_m)[lp]);
+__device__ __forceinline__ uint32_t load_header_word(const KParams& p, int64_t lp, int lane) {
+  constexpr int WT = sizeof(T) / 4;  // words per scalar
+  const uint32_t* base;
+  int64_t wi;
+  if (lane == 0) {
+    base = reinterpret_cast<const uint32_t*>(p.m);
+    wi = lp;
+  } else if (lane < 5) {
+    base = reinterpret_cast<const uint32_t*>(p.offset);
+    wi = 2 * lp + (lane - 1);  // offset[lp], offset[lp+1] as lo/hi words
+  } else if (lane < 5 + 2 * WT) {
+    base = reinterpret_cast<const uint32_t*>(p.c);
+    wi = 2 * WT * lp + (lane - 5);
+  } else {
+    base = reinterpret_cast<const uint32_t*>(p.bound_m);
+    wi = WT * lp + (lane - 5 - 2 * WT);
+  }
+  const bool on = lp >= 0 && lane < 5 + 3 * WT;
+  return ldg_u32_if(base + (on ? wi : 0), on);
+}
+
+template <typename T>
+__device__ __forceinline__ T word_scalar(uint32_t w, int src) {
+  if constexpr (sizeof(T) == 4) {
+    return __uint_as_float(__shfl_sync(kFull, w, src));
+  } else {
+    const uint32_t lo = __shfl_sync(kFull, w, src), hi = __shfl_sync(kFull, w, src + 1);
+    return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
   }
 }
 
 template <typename L, typename T>
-__device__ __forceinline__ Header<T> unpack_header(uint64_t f) {
+__device__ __forceinline__ Header<T> unpack_header(uint32_t w, int64_t lp) {
+  constexpr int WT = sizeof(T) / 4;
   Header<T> h;
-  h.lp = (int64_t)__shfl_sync(kFull, f, 0);
-  h.m = (int32_t)(uint32_t)__shfl_sync(kFull, f, 1);
-  h.off = (int64_t)__shfl_sync(kFull, f, 2);
-  const int64_t o1 = (int64_t)__shfl_sync(kFull, f, 3);
-  h.cx = from_bits64<T>(__shfl_sync(kFull, f, 4));
-  h.cy = from_bits64<T>(__shfl_sync(kFull, f, 5));
-  h.M = from_bits64<T>(__shfl_sync(kFull, f, 6));
+  h.lp = lp;
+  h.m = (int32_t)__shfl_sync(kFull, w, 0);
+  h.off = (int64_t)(((uint64_t)__shfl_sync(kFull, w, 2) << 32) | __shfl_sync(kFull, w, 1));
+  const int64_t o1 = (int64_t)(((uint64_t)__shfl_sync(kFull, w, 4) << 32) | __shfl_sync(kFull, w, 3));
+  h.cx = word_scalar<T>(w, 5);
+  h.cy = word_scalar<T>(w, 5 + WT);
+  h.M = word_scalar<T>(w, 5 + 2 * WT);
   const int64_t cap8 = ((int64_t)h.m + 7) & ~int64_t(7);
   h.ok = h.m >= 0 && h.m <= L::kCap && (h.off & 7) == 0 && o1 - h.off >= cap8;
   return h;
@@ -521,19 +560,29 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
   const int64_t TW = p.total_warps;
   const int64_t j0 = (int64_t)blockIdx.x * W + wic;
   auto lp_of = [&](int64_t t) -> int64_t { return t < n_list ? (list ? (int64_t)list[t] : t) : -1; };
-  uint64_t hA = load_header_field<T>(p, lp_of(j0), lane);       // LP being solved
-  uint64_t hB = load_header_field<T>(p, lp_of(j0 + TW), lane);  // LP being staged
-  int64_t ticket = 0;
-  if (lane == 0) ticket = (int64_t)atomicAdd(p.counter, 1u) + 2 * TW;
-  Header<T> h = unpack_header<L, T>(hA);
+  int64_t lpA = lp_of(j0), lpB = lp_of(j0 + TW);
+  uint32_t hA = load_header_word<T>(p, lpA, lane);  // LP being solved
+  uint32_t hB = load_header_word<T>(p, lpB, lane);  // LP being staged
+  uint32_t ticket = atomic_add_if(p.counter, lane == 0);
+  Header<T> h = unpack_header<L, T>(hA, lpA);
   if (lane == 0 && h.lp >= 0) issue_tma<L, T, P>(p, h, buf, bar, policy);
   // deferred pair export of the previous LP (lanes 0 and 1)
   int64_t pend_lp = -1;
   uint32_t pend_pos = kNone, pend_q = 0;
 
+#ifdef LP2D_PROFILE_WAIT
+  long long prof_wait = 0;
+  const long long prof_t0 = clock64();
+#endif
   while (h.lp >= 0) {
+#ifdef LP2D_PROFILE_WAIT
+    const long long tw0 = clock64();
+#endif
     mbar_wait(bar, phase);
     phase ^= 1u;
+#ifdef LP2D_PROFILE_WAIT
+    prof_wait += clock64() - tw0;
+#endif
 
     // ---- gather: chunk K of the insertion order into registers / the tail --
     // Out-of-range perm entries are clamped for the load and reported through
@@ -558,7 +607,7 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
       T vax = valid ? sax[oc] : T(0);
       T vay = valid ? say[oc] : T(0);
       T vb = valid ? sb[oc] : T(INFINITY);
-      sbits = max(sbits, float_bits(fabs(vax) + fabs(vay)));
+      if constexpr (NT == 0) sbits = max(sbits, float_bits(fabs(vax) + fabs(vay)));
       if (K == 0 && P_ < 4) {
         vax = P_ == 0 ? T(1) : (P_ == 1 ? T(-1) : T(0));
         vay = P_ == 2 ? T(1) : (P_ == 3 ? T(-1) : T(0));
@@ -568,16 +617,26 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
       ray[K] = vay;
       rb[K] = vb;
     }
-    if constexpr (NT > 0) {  // tail: validate and bound only (read in place later)
+    if constexpr (NT > 0) {
+      // Tail: validate the permutation only (read in place later) ...
 #pragma unroll 1
       for (int c = 0; c < NT && 32 * (NS + c) < mpos; ++c) {
         const int P_ = 32 * (NS + c) + lane;
-        if (P_ < mpos) {
-          const uint32_t o = sperm[P_ - 4];
-          pmax = max(pmax, o);
-          const uint32_t oc = min(o, (uint32_t)(L::kCap - 1));
-          sbits = max(sbits, float_bits(fabs(sax[oc]) + fabs(say[oc])));
-        }
+        if (P_ < mpos) pmax = max(pmax, (uint32_t)sperm[P_ - 4]);
+      }
+      // ... and bound max |ax|+|ay| over the whole LP in ORIGINAL order with
+      // 16-byte vector loads (order-independent, conflict-free).
+      constexpr int V = 16 / sizeof(T);
+#pragma unroll 1
+      for (int i = lane * V; i < mj; i += 32 * V) {
+        typedef typename std::conditional<sizeof(T) == 4, float4, double2>::type VecT;
+        const VecT vx = *reinterpret_cast<const VecT*>(sax + i);
+        const VecT vy = *reinterpret_cast<const VecT*>(say + i);
+        const T* xs = reinterpret_cast<const T*>(&vx);
+        const T* ys = reinterpret_cast<const T*>(&vy);
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+          if (i + e < mj) sbits = max(sbits, float_bits(fabs(xs[e]) + fabs(ys[e])));
       }
     }
     const bool bad = !h.ok || (mj > 0 && __reduce_max_sync(kFull, pmax) >= (uint32_t)mj);
@@ -585,12 +644,13 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
     fence_proxy_async_smem();
 
     // ---- advance the pipeline (all inputs were requested an LP ago) --------
-    const Header<T> hn = unpack_header<L, T>(hB);
+    const Header<T> hn = unpack_header<L, T>(hB, lpB);
     if constexpr (!L::kLateTma)
       if (lane == 0 && hn.lp >= 0) issue_tma<L, T, P>(p, hn, buf, bar, policy);
-    const int64_t tk = __shfl_sync(kFull, ticket, 0);
-    hB = load_header_field<T>(p, lp_of(tk), lane);
-    if (lane == 0) ticket = (int64_t)atomicAdd(p.counter, 1u) + 2 * TW;
+    const int64_t tk = (int64_t)__shfl_sync(kFull, ticket, 0) + 2 * TW;
+    lpB = lp_of(tk);
+    hB = load_header_word<T>(p, lpB, lane);
+    ticket = atomic_add_if(p.counter, lane == 0);
     if (pend_lp >= 0 && lane < 2 && p.pair) p.pair[2 * pend_lp + lane] = pair_code(pend_pos, pend_q);
 
     // Per-LP parallel-test bound (see wu_fold), never below the fast
@@ -721,13 +781,23 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
     pend_lp = h.lp;
     pend_pos = lane == 0 ? S.pos0 : S.pos1;
     if (st == 255) pend_pos = kNone;
-    pend_q = 0;
-    if (lane < 2 && pend_pos != kNone && pend_pos >= 4)
-      pend_q = static_cast<const P*>(p.perm)[h.off + pend_pos - 4];
+    {
+      const bool need = lane < 2 && pend_pos != kNone && pend_pos >= 4;
+      const P* pa = static_cast<const P*>(p.perm) + h.off + (need ? pend_pos - 4 : 0);
+      pend_q = sizeof(P) == 2 ? ldg_u16_if(pa, need) : ldg_u32_if(pa, need);
+    }
     h = hn;
   }
   if (pend_lp >= 0 && lane < 2 && p.pair) p.pair[2 * pend_lp + lane] = pair_code(pend_pos, pend_q);
 
+#ifdef LP2D_PROFILE_WAIT
+  if (lane == 0 && p.wu) {  // debug: per-warp [wait cycles, total cycles] into wu[]
+    const int64_t gw = (int64_t)blockIdx.x * W + wic;
+    atomicAdd((unsigned long long*)&p.wu[0], (unsigned long long)prof_wait);
+    atomicAdd((unsigned long long*)&p.wu[1], (unsigned long long)(clock64() - prof_t0));
+    (void)gw;
+  }
+#endif
   // Self-reset of the ticket counter by the last warp to finish, so the next
   // launch on this counter slot starts from zero without a memset.
   if (lane == 0) {
