@@ -44,11 +44,15 @@ sys.path.insert(0, ROOT)
 METRIC = "LPs solved/sec at 16384 LPs x 1024 constraints; achieved HBM GB/s vs peak"
 
 CONFIGS = {
-    # name: (per-GPU LPs, m, dtype, seed, description)
+    # name: (per-GPU LPs, m, dtype, seed, description); m = 0: heavy-tailed sizes
     "c1": (1024, 64, np.float32, 1, "1024 LPs x 64 constraints fp32 (BASELINE configs[0])"),
     "c2": (16384, 1024, np.float32, 2, "16384 LPs x 1024 constraints fp32 (BASELINE configs[1])"),
-    "c3": (1 << 17, 128, np.float32, 3, "2^20 LPs x 128 constraints fp32 sharded over 8 GPUs: 2^17 per GPU (BASELINE configs[2])"),
-    "c5": (1 << 19, 256, np.float64, 5, "2^22 LPs x 256 constraints fp64 sharded over 8 GPUs: 2^19 per GPU (BASELINE configs[4])"),
+    "c3": (1 << 17, 128, np.float32, 3, "2^20 LPs x 128 constraints fp32 ORCA-style (|v|<=2 rescale, "
+           "every 10th infeasible) sharded over 8 GPUs: 2^17 per GPU (BASELINE configs[2])"),
+    "c4": (0, 0, np.float32, 4, "mixed batch, Pareto(x_min 8, alpha 1) sizes clamped to 8..8192, "
+           "sum m ~ 2^24 per GPU, fp32 (BASELINE configs[3])"),
+    "c5": (1 << 19, 256, np.float64, 5, "2^22 LPs x 256 constraints fp64, 10% infeasible + 10% unbounded, "
+           "sharded over 8 GPUs: 2^19 per GPU (BASELINE configs[4])"),
 }
 
 
@@ -130,12 +134,34 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def pareto_sizes(seed, total=1 << 24):
+    import paper_1902_04995_b200 as P
+
+    out = np.zeros(total // 8 + 1, np.int32)
+    k = P.lp2d.N.lib().lp2dgen_pareto_sizes(seed, 8.0, 1.0, 8192, total, len(out), out.ctypes.data)
+    return out[:k]
+
+
 def make_batch(cfg_name, rank):
+    """SURVEY.md §8(d) workloads; LP j of rank r is global LP r*n + j."""
     import paper_1902_04995_b200 as P
 
     n, m, dt, seed, _ = CONFIGS[cfg_name]
-    sizes = np.full(n, m, np.int32)
-    pb = P.PackedBatch.generate(sizes, seed, first=rank * n)
+    kind, bscale = None, 1.0
+    if cfg_name == "c4":
+        sizes = pareto_sizes(seed)
+        n = len(sizes)
+    else:
+        sizes = np.full(n, m, np.int32)
+    g = np.arange(rank * n, (rank + 1) * n)
+    if cfg_name == "c3":
+        kind = np.where(g % 10 == 0, P.GenKind.infeasible, P.GenKind.feasible_random).astype(np.uint8)
+        bscale = 2e-7
+    elif cfg_name == "c5":
+        kind = np.full(n, int(P.GenKind.feasible_random), np.uint8)
+        kind[g % 10 == 3] = int(P.GenKind.infeasible)
+        kind[g % 10 == 7] = int(P.GenKind.unbounded_random)
+    pb = P.PackedBatch.generate(sizes, seed, first=rank * n, kind=kind, bscale=bscale)
     return pb.astype(dt) if dt != np.float64 else pb
 
 
@@ -166,8 +192,13 @@ def cpu_reference(pb, steps, warmup, threads=0):
         ref.ref_batch_free(h)
     total_s = sum(ns) / 1e9
     return {"value": n * steps / total_s, "unit": "LPs/s", "cores": cores, "kind": "reference",
-            "sample": f"{n} LPs x {int(pb.m[0])} constraints, fp64 solve_batch(balanced, width 512, "
+            "sample": f"{n} LPs x {sizes_desc(pb)} constraints, fp64 solve_batch(balanced, width 512, "
                       f"{cores} workers) x {steps} runs = {total_s:.2f} s wall"}
+
+
+def sizes_desc(pb):
+    lo, hi = int(pb.m.min()), int(pb.m.max())
+    return str(lo) if lo == hi else f"{lo}..{hi} (mean {pb.m.mean():.1f})"
 
 
 def run_reference_arm(args, world, rank):
@@ -176,6 +207,7 @@ def run_reference_arm(args, world, rank):
     if rank != 0:
         return
     pb = make_batch(cfg, 0)
+    n, m = pb.n, (m or int(pb.m.mean()))
     cb = cpu_reference(pb, args.steps, args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "LPs/s",
@@ -230,6 +262,7 @@ def main():
     cfg = args.config
     n, m, dt, seed, desc = CONFIGS[cfg]
     pb = make_batch(cfg, rank)
+    n, m = pb.n, (m or int(pb.m.mean()))
     algo_bytes = pb.constraint_bytes()
 
     # ---- device-resident kernel timing ----------------------------------------
@@ -260,6 +293,22 @@ def main():
     ms_per_step = region_ms / args.steps
     value = world * n / (ms_per_step / 1e3)
     gpu_launches = args.steps  # one solve kernel per step
+
+    # ---- naive scheduler on the same device batch (paper's RGB-naive vs
+    # balanced comparison) ------------------------------
+    naive = P.BlockConfig(scheduler=P.SchedulerKind.naive)
+    for _ in range(2):
+        P.solve_device(db, out, naive, stream=stream)
+    ne0 = torch.cuda.Event(enable_timing=True)
+    ne1 = torch.cuda.Event(enable_timing=True)
+    nsteps = 3
+    ne0.record(stream)
+    for _ in range(nsteps):
+        P.solve_device(db, out, naive, stream=stream)
+    ne1.record(stream)
+    torch.cuda.synchronize()
+    naive_ms = ne0.elapsed_time(ne1) / nsteps
+    P.solve_device(db, out, stream=stream)  # leave balanced results in `out`
 
     # ---- end-to-end through the C ABI with pinned host buffers ---------------
     e2e_steps = args.e2e_steps or min(args.steps, 5)
@@ -304,6 +353,10 @@ def main():
             "e2e": {"value": e2e_value, "unit": "LPs/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
             "gpu_launches": gpu_launches,
+            "schedulers": {"balanced_kernel_ms": kern_ms, "naive_kernel_ms": naive_ms,
+                           "naive_over_balanced": naive_ms / kern_ms,
+                           "note": "naive = thread per LP (paper's RGB naive), balanced = "
+                                   "warp-dealt work units (this kernel); same device batch"},
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:

@@ -50,6 +50,10 @@ struct DeviceState {
   void* arena = nullptr;
   size_t arena_bytes = 0;
   cudaStream_t stream = nullptr;
+  // fork/join of size-class launches (mixed batches)
+  std::mutex fork_mu;
+  cudaStream_t cls_stream[16] = {};
+  cudaEvent_t cls_event[17] = {};
 };
 
 DeviceState g_dev[64];
@@ -71,6 +75,8 @@ int ensure_device(int dev) {
   CUDA_TRY(cudaMalloc(&d.counters, sizeof(uint32_t) * 2 * kCounterSlots));
   CUDA_TRY(cudaMemset(d.counters, 0, sizeof(uint32_t) * 2 * kCounterSlots));
   CUDA_TRY(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+  for (auto& cs : d.cls_stream) CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  for (auto& ce : d.cls_event) CUDA_TRY(cudaEventCreateWithFlags(&ce, cudaEventDisableTiming));
   CUDA_TRY(cudaDeviceSynchronize());
   d.init = true;
   return 0;
@@ -160,9 +166,34 @@ int launch_global_kernel(KParams kp, int dev, cudaStream_t stream) {
   return 0;
 }
 
+// Large class: CTA per LP with the LP in shared memory (k_solve_cta); the
+// smem capacity covers the class's largest LP up to ~200 KB, bigger LPs are
+// solved by the CTA's warp 0 from global memory.
 template <typename T, typename P>
-int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s) {
-  if (cls >= n_reg_classes<T>()) return launch_global_kernel<T, P>(kp, dev, s);
+int launch_cta_kernel(KParams kp, int64_t max_m, int dev, cudaStream_t stream) {
+  auto kern = k_solve_cta<T, P>;
+  const size_t head = (sizeof(CtaShared<T>) + 127) & ~size_t(127);
+  const size_t max_bytes = 200 * 1024;
+  int64_t cap = ((max_m + 4 + 255) / 256) * 256;
+  const int64_t cap_max = (int64_t)((max_bytes - head) / (3 * sizeof(T))) & ~int64_t(255);
+  cap = std::min(cap, cap_max);
+  const size_t smem = head + 3 * sizeof(T) * (size_t)cap;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int b = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kCtaThreads, smem));
+  b = std::max(b, 1);
+  const int64_t maxb = (int64_t)b * g_dev[dev].sm_count;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kp.n_list, maxb));
+  kp.total_warps = grid;
+  kp.counter = take_counter(dev);
+  kern<<<grid, kCtaThreads, smem, stream>>>(kp, (int32_t)cap);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <typename T, typename P>
+int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t max_m) {
+  if (cls >= n_reg_classes<T>()) return launch_cta_kernel<T, P>(kp, max_m, dev, s);
   switch (kSlotClasses[cls]) {
     case 1: return launch_warp_kernel<T, P, 1>(kp, dev, s);
     case 2: return launch_warp_kernel<T, P, 2>(kp, dev, s);
@@ -185,7 +216,7 @@ int launch_balanced(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStrea
                     bool may_sync) {
   const int cmin = class_of<T>(std::max<int64_t>(min_m, 0));
   const int cmax = class_of<T>(max_m);
-  if (cmin == cmax) return launch_class<T, P>(kp, cmax, dev, s);
+  if (cmin == cmax) return launch_class<T, P>(kp, cmax, dev, s, max_m);
   // Mixed sizes: bin LP ids by class on the device, one launch per class.
   BinSpec spec{};
   spec.nreg = n_reg_classes<T>();
@@ -211,13 +242,24 @@ int launch_balanced(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStrea
     CUDA_TRY(cudaStreamSynchronize(s));
   }
   int rc = 0;
+  // One stream per class, forked from and joined back into s: a class's
+  // tail (few long LPs) overlaps the next classes instead of idling the GPU.
   // Largest class first: its LPs are the longest, so they start earliest.
-  for (int c = cmax; c >= cmin && rc == 0; --c) {
-    if (may_sync && host_counts[c] == 0) continue;
-    KParams kc = kp;
-    kc.bin_class = c;
-    if (may_sync) kc.n_list = host_counts[c];
-    rc = launch_class<T, P>(kc, c, dev, s);
+  {
+    DeviceState& d = g_dev[dev];
+    std::lock_guard<std::mutex> lock(d.fork_mu);
+    CUDA_TRY(cudaEventRecord(d.cls_event[16], s));
+    for (int c = cmax; c >= cmin && rc == 0; --c) {
+      if (may_sync && host_counts[c] == 0) continue;
+      KParams kc = kp;
+      kc.bin_class = c;
+      if (may_sync) kc.n_list = host_counts[c];
+      cudaStream_t cs = d.cls_stream[c];
+      CUDA_TRY(cudaStreamWaitEvent(cs, d.cls_event[16], 0));
+      rc = launch_class<T, P>(kc, c, dev, cs, max_m);
+      CUDA_TRY(cudaEventRecord(d.cls_event[c], cs));
+      CUDA_TRY(cudaStreamWaitEvent(s, d.cls_event[c], 0));
+    }
   }
   CUDA_TRY(cudaFreeAsync(ws, s));
   return rc;

@@ -902,6 +902,238 @@ __global__ void __launch_bounds__(128) k_solve_naive(const KParams p) {
   write_result<T, P>(p, h, st, px, py, pos0, pos1, viol, wu);
 }
 
+// ---------------------------------------------------------------------------
+// Large LPs: one CTA (kCtaThreads threads) per LP. The LP is gathered once
+// from global memory through its permutation into shared memory in insertion
+// order (positions 0..3 = box), then
+//   * the violation test sweeps kCtaThreads positions per step (warp ballots
+//     combined through shared memory, first violated position wins);
+//   * a violation's 1D re-solve deals the prefix round-robin over ALL threads
+//     of the CTA (the reference's balanced deal with the CTA as the block,
+//     batch.hpp:219-240), lanes fold branch-free (wu_fold), warps merge with
+//     REDUX and the 8 warp results are merged through shared memory;
+//   * every thread resolves the event redundantly (identical inputs and
+//     operations), so the new optimum needs no broadcast.
+// LPs whose size exceeds the launch's shared-memory capacity, or whose
+// magnitudes leave the fast path's range, are solved by warp 0 with
+// solve_exact_global.
+constexpr int kCtaThreads = 128;
+constexpr int kCtaWarps = kCtaThreads / 32;
+
+template <typename T>
+struct CtaShared {
+  T vL[kCtaWarps], vR[kCtaWarps];  // per-warp merged interval endpoints
+  int64_t lp_next;
+  uint32_t oL[kCtaWarps], oR[kCtaWarps], par[kCtaWarps];
+  uint32_t bal[kCtaWarps];         // per-warp violation ballots of a test step
+  uint32_t redk[kCtaWarps][3];     // per-warp pmax / |a| bound words
+};
+
+template <typename T, typename P>
+__global__ void __launch_bounds__(kCtaThreads) k_solve_cta(const KParams p, int32_t cap_pos) {
+  static_assert(sizeof(T) == 4 || sizeof(T) == 8, "scalar");
+  extern __shared__ __align__(128) unsigned char smem[];
+  CtaShared<T>& sh = *reinterpret_cast<CtaShared<T>*>(smem);
+  T* pax = reinterpret_cast<T*>(smem + ((sizeof(CtaShared<T>) + 127) & ~size_t(127)));
+  T* pay = pax + cap_pos;
+  T* pb = pay + cap_pos;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int32_t* list;
+  int64_t n_list;
+  resolve_list(p, list, n_list);
+  const T eps_par = Eps<T>::par(p);
+  const T eps_feas = Eps<T>::feas(p);
+  const T eps_hi = Eps<T>::hi(p);
+  int64_t j = blockIdx.x;
+  while (j < n_list) {
+    Header<T> h;
+    h.lp = list ? (int64_t)list[j] : j;
+    h.m = p.m[h.lp];
+    h.off = p.offset[h.lp];
+    h.ok = h.m >= 0;
+    h.cx = static_cast<const T*>(p.c)[2 * h.lp];
+    h.cy = static_cast<const T*>(p.c)[2 * h.lp + 1];
+    h.M = static_cast<const T*>(p.bound_m)[h.lp];
+    if (tid == 0) sh.lp_next = (int64_t)atomicAdd(p.counter, 1u) + gridDim.x;
+    const int mpos = h.m + 4;
+    const bool fits = h.ok && mpos <= cap_pos;
+    // ---- gather (global -> shared, insertion order) ----------------------
+    uint32_t pmax = 0;
+    decltype(float_bits(T(0))) sbits = float_bits(T(1));
+    const T* gax = static_cast<const T*>(p.ax) + h.off;
+    const T* gay = static_cast<const T*>(p.ay) + h.off;
+    const T* gb = static_cast<const T*>(p.b) + h.off;
+    const P* gperm = static_cast<const P*>(p.perm) + h.off;
+    if (fits) {
+      if (tid < 4) {
+        pax[tid] = tid == 0 ? T(1) : (tid == 1 ? T(-1) : T(0));
+        pay[tid] = tid == 2 ? T(1) : (tid == 3 ? T(-1) : T(0));
+        pb[tid] = h.M;
+      }
+      // Random gathers from L2/HBM: batches of 8 independent chains per
+      // thread keep enough loads in flight to cover the latency.
+      constexpr int U = 8;
+      for (int i0 = tid; i0 < h.m; i0 += U * kCtaThreads) {
+        uint32_t o[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * kCtaThreads;
+          o[u] = i < h.m ? (uint32_t)gperm[i] : 0u;
+        }
+        T vx[U], vy[U], vb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          pmax = max(pmax, o[u]);
+          const uint32_t oc = min(o[u], (uint32_t)(h.m - 1));
+          vx[u] = gax[oc];
+          vy[u] = gay[oc];
+          vb[u] = gb[oc];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * kCtaThreads;
+          if (i < h.m) {
+            sbits = max(sbits, float_bits(fabs(vx[u]) + fabs(vy[u])));
+            pax[4 + i] = vx[u];
+            pay[4 + i] = vy[u];
+            pb[4 + i] = vb[u];
+          }
+        }
+      }
+    } else if (h.ok) {
+      for (int i = tid; i < h.m; i += kCtaThreads) pmax = max(pmax, (uint32_t)gperm[i]);
+    }
+    // block reductions of pmax / sbits (as 32-bit words: max of the high
+    // word then of the low word is the max of the bits for both types)
+    pmax = __reduce_max_sync(kFull, pmax);
+    const auto sb_w = reduce_max_bits(sbits);
+    if (lane == 0) {
+      sh.redk[wid][0] = pmax;
+      sh.redk[wid][1] = (uint32_t)((unsigned long long)sb_w >> (sizeof(T) == 8 ? 32 : 0));
+      sh.redk[wid][2] = (uint32_t)(unsigned long long)sb_w;
+    }
+    __syncthreads();
+    uint32_t pm_all = 0;
+    decltype(float_bits(T(0))) sb_all = 0;
+    for (int w = 0; w < kCtaWarps; ++w) {
+      pm_all = max(pm_all, sh.redk[w][0]);
+      decltype(float_bits(T(0))) v;
+      if constexpr (sizeof(T) == 8) v = ((unsigned long long)sh.redk[w][1] << 32) | sh.redk[w][2];
+      else v = sh.redk[w][2];
+      sb_all = max(sb_all, v);
+    }
+    const bool bad = !h.ok || (h.m > 0 && pm_all >= (uint32_t)h.m);
+    const T m_all = float_from_bits<T>(sb_all);
+    const bool wild = !(m_all < Limits<T>::kBig) || !(fabs(h.M) < T(INFINITY)) || !fits;
+    const T lpbnd = fmax(fmax(m_all, Limits<T>::kSmall) * eps_hi, FastDiv<T>::kDLo);
+    LPState<T> S;
+    lp_init(S, h);
+    S.st = bad ? 255 : 0;
+    const T cthr = eps_par * sqrt(h.cx * h.cx + h.cy * h.cy);
+    bool need_exact = !bad && wild;
+    // ---- sweep -------------------------------------------------------------
+    int start = 4;  // first position to test
+    bool running = !bad && !wild;
+    while (running) {
+      int pi = -1;
+      for (int base = start & ~(kCtaThreads - 1); base < mpos; base += kCtaThreads) {
+        const int P_ = base + tid;
+        const bool v = P_ >= start && P_ < mpos &&
+                       !satisfied(pax[P_], pay[P_], pb[P_], S.px, S.py, eps_feas);
+        const uint32_t bm = __ballot_sync(kFull, v);
+        __syncthreads();  // previous step's readers of sh.bal are done
+        if (lane == 0) sh.bal[wid] = bm;
+        __syncthreads();
+        for (int w = 0; w < kCtaWarps; ++w) {
+          const uint32_t b = sh.bal[w];
+          if (b) {
+            pi = base + 32 * w + __ffs(b) - 1;
+            break;
+          }
+        }
+        if (pi >= 0) break;
+      }
+      if (pi < 0) break;
+      // ---- event at position pi ------------------------------------------
+      S.viol += 1;
+      S.wu += (uint32_t)pi;
+      const Line<T> l = boundary_of(pax[pi], pay[pi], pb[pi]);
+      Acc<T> acc;
+      acc.uL = -T(INFINITY);
+      acc.uR = T(INFINITY);
+      acc.oL = acc.oR = acc.par = kNone;
+      bool rare = false;
+      for (int k = tid; k < pi; k += kCtaThreads)
+        wu_fold(pax[k], pay[k], pb[k], l, lpbnd, (uint32_t)k, true, acc, rare);
+      bool rare_cta = __syncthreads_or(rare);
+      if (rare_cta) {  // exact reference classify for every unit (rare)
+        acc.uL = -T(INFINITY);
+        acc.uR = T(INFINITY);
+        acc.oL = acc.oR = acc.par = kNone;
+        for (int k = tid; k < pi; k += kCtaThreads)
+          wu_apply(pax[k], pay[k], pb[k], l, eps_par, eps_feas, eps_hi, (uint32_t)k, acc);
+      }
+      const Merged<T> mw = merge_lanes(acc, true);
+      if (lane == 0) {
+        sh.vL[wid] = mw.uL;
+        sh.vR[wid] = mw.uR;
+        sh.oL[wid] = mw.oL;
+        sh.oR[wid] = mw.oR;
+        sh.par[wid] = mw.par;
+      }
+      __syncthreads();
+      // Merge the warps' extremes (value equality ties keep the smaller
+      // position, as the serial fold does).
+      Merged<T> mg;
+      mg.uL = -T(INFINITY);
+      mg.uR = T(INFINITY);
+      mg.oL = mg.oR = mg.par = kNone;
+      for (int w = 0; w < kCtaWarps; ++w) {
+        const T vl = sh.vL[w], vr = sh.vR[w];
+        if (vl > mg.uL) {
+          mg.uL = vl;
+          mg.oL = sh.oL[w];
+        } else if (vl == mg.uL) {
+          mg.oL = min(mg.oL, sh.oL[w]);
+        }
+        if (vr < mg.uR) {
+          mg.uR = vr;
+          mg.oR = sh.oR[w];
+        } else if (vr == mg.uR) {
+          mg.oR = min(mg.oR, sh.oR[w]);
+        }
+        mg.par = min(mg.par, sh.par[w]);
+      }
+      __syncthreads();  // the shared merge slots are reused by the next event
+      if (!resolve_merged(S, mg, l, (uint32_t)pi, h, cthr, eps_feas)) break;
+      if (!(fabs(S.px) < T(INFINITY) && fabs(S.py) < T(INFINITY))) {
+        need_exact = true;
+        break;
+      }
+      start = pi + 1;
+    }
+    if (need_exact) {
+      if (wid == 0) solve_exact_global<T, P>(p, h, eps_par, eps_feas, eps_hi, S);
+    }
+    if (tid == 0) {
+      uint8_t st = S.st;
+      if (st == 0 && (S.pos0 < 4 || S.pos1 < 4)) st = 2;
+      write_result<T, P>(p, h, st, S.px, S.py, S.pos0, S.pos1, S.viol, S.wu);
+    }
+    __syncthreads();
+    j = sh.lp_next;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    __threadfence();
+    const uint32_t t = atomicAdd(p.counter + 1, 1u);
+    if (t == gridDim.x - 1) {
+      p.counter[0] = 0;
+      p.counter[1] = 0;
+    }
+  }
+}
+
 // Large LPs (m above the register classes) and any other LP: one warp per
 // LP straight from global memory (solve_exact_global), claimed dynamically.
 template <typename T, typename P>
