@@ -9,5 +9,6 @@ from .lp2d import (  # noqa: F401
     identity_permutation, lane_imbalance, replicate, shuffle, solve_batch, solve_device,
     solve_packed,
 )
+from .lp2d import ParseError, problem_from_text, to_text  # noqa: F401  (io.hpp)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

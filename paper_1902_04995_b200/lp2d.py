@@ -461,3 +461,67 @@ def agree_sig_figs(a: float, b: float, sig_figs: int = 5) -> bool:
     mag = max(abs(a), abs(b))
     step = 10.0 ** (math.floor(math.log10(mag)) - (sig_figs - 1))
     return abs(a - b) <= 0.5 * step
+
+
+# ---- lp2d v1 text instances (io.hpp:13-97), for replaying single LPs -------
+
+class ParseError(RuntimeError):
+    """io.hpp read_problem throws std::runtime_error("lp2d parse: ...")."""
+
+
+def _full(v: float) -> str:
+    return "%.16e" % v  # io.hpp:28-32 full_precision: bit-exact round trip
+
+
+def to_text(p: Problem) -> str:
+    """io.hpp:34-47 write_problem / to_text."""
+    out = [f"lp2d v1 m={p.constraints.shape[0]} M={_full(p.bound_m)}",
+           f"c {_full(p.c[0])} {_full(p.c[1])}"]
+    for ax, ay, b in p.constraints:
+        out.append(f"h {_full(ax)} {_full(ay)} {_full(b)}")
+    return "\n".join(out) + "\n"
+
+
+def problem_from_text(text: str) -> Problem:
+    """io.hpp:49-97 read_problem: same checks, same failure cases."""
+    import math
+
+    tok = text.split()
+
+    def fail(what):
+        raise ParseError("lp2d parse: " + what)
+
+    if (len(tok) < 4 or tok[0] != "lp2d" or tok[1] != "v1" or not tok[2].startswith("m=")
+            or not tok[3].startswith("M=")):
+        fail("bad header line")
+    try:
+        m = int(tok[2][2:])
+        bound = float(tok[3][2:])
+    except ValueError:
+        fail("bad header numbers")
+    if m < 0:
+        fail("bad header numbers")
+    if not math.isfinite(bound) or bound <= 0.0:
+        fail("bound must be positive and finite")
+    try:
+        if tok[4] != "c":
+            fail("bad objective line")
+        c = (float(tok[5]), float(tok[6]))
+    except (IndexError, ValueError):
+        fail("bad objective line")
+    if not (math.isfinite(c[0]) and math.isfinite(c[1])):
+        fail("objective not finite")
+    rows = []
+    pos = 7
+    for _ in range(m):
+        try:
+            if tok[pos] != "h":
+                fail("bad constraint line")
+            ax, ay, b = float(tok[pos + 1]), float(tok[pos + 2]), float(tok[pos + 3])
+        except (IndexError, ValueError):
+            fail("bad constraint line")
+        pos += 4
+        if not all(math.isfinite(v) for v in (ax, ay, b)) or (ax == 0.0 and ay == 0.0):
+            fail("constraint not finite or zero normal")  # core.hpp:41-43 valid()
+        rows.append((ax, ay, b))
+    return Problem(c, np.array(rows, dtype=np.float64).reshape(-1, 3), bound)
