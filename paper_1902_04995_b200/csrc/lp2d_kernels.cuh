@@ -560,10 +560,15 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
   const int64_t TW = p.total_warps;
   const int64_t j0 = (int64_t)blockIdx.x * W + wic;
   auto lp_of = [&](int64_t t) -> int64_t { return t < n_list ? (list ? (int64_t)list[t] : t) : -1; };
-  int64_t lpA = lp_of(j0), lpB = lp_of(j0 + TW);
+  // With the late TMA (NT > 0) the next LP's data is only requested at the
+  // end of the current solve, so one LP of lookahead suffices: the ticket is
+  // claimed when the current solve starts. A deeper pipeline would leave
+  // claimed-but-unstarted LPs behind slow warps at the end of the batch.
+  constexpr int64_t kAhead = L::kLateTma ? 1 : 2;
+  int64_t lpA = lp_of(j0), lpB = L::kLateTma ? -1 : lp_of(j0 + TW);
   uint32_t hA = load_header_word<T>(p, lpA, lane);  // LP being solved
-  uint32_t hB = load_header_word<T>(p, lpB, lane);  // LP being staged
-  uint32_t ticket = atomic_add_if(p.counter, lane == 0);
+  uint32_t hB = L::kLateTma ? 0u : load_header_word<T>(p, lpB, lane);  // LP being staged
+  uint32_t ticket = L::kLateTma ? 0u : atomic_add_if(p.counter, lane == 0);
   Header<T> h = unpack_header<L, T>(hA, lpA);
   if (lane == 0 && h.lp >= 0) issue_tma<L, T, P>(p, h, buf, bar, policy);
   // deferred pair export of the previous LP (lanes 0 and 1)
@@ -575,6 +580,7 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
   const long long prof_t0 = clock64();
 #endif
   while (h.lp >= 0) {
+    if constexpr (L::kLateTma) ticket = atomic_add_if(p.counter, lane == 0);
 #ifdef LP2D_PROFILE_WAIT
     const long long tw0 = clock64();
 #endif
@@ -582,6 +588,10 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
     phase ^= 1u;
 #ifdef LP2D_PROFILE_WAIT
     prof_wait += clock64() - tw0;
+#endif
+#ifdef LP2D_PROFILE_TIMELINE
+    uint64_t tl_t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_t0));
 #endif
 
     // ---- gather: chunk K of the insertion order into registers / the tail --
@@ -644,13 +654,15 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
     fence_proxy_async_smem();
 
     // ---- advance the pipeline (all inputs were requested an LP ago) --------
-    const Header<T> hn = unpack_header<L, T>(hB, lpB);
-    if constexpr (!L::kLateTma)
+    Header<T> hn;
+    if constexpr (!L::kLateTma) {
+      hn = unpack_header<L, T>(hB, lpB);
       if (lane == 0 && hn.lp >= 0) issue_tma<L, T, P>(p, hn, buf, bar, policy);
-    const int64_t tk = (int64_t)__shfl_sync(kFull, ticket, 0) + 2 * TW;
+    }
+    const int64_t tk = (int64_t)__shfl_sync(kFull, ticket, 0) + kAhead * TW;
     lpB = lp_of(tk);
     hB = load_header_word<T>(p, lpB, lane);
-    ticket = atomic_add_if(p.counter, lane == 0);
+    if constexpr (!L::kLateTma) ticket = atomic_add_if(p.counter, lane == 0);
     if (pend_lp >= 0 && lane < 2 && p.pair) p.pair[2 * pend_lp + lane] = pair_code(pend_pos, pend_q);
 
     // Per-LP parallel-test bound (see wu_fold), never below the fast
@@ -772,11 +784,23 @@ __global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
     if constexpr (L::kLateTma) {  // the tail lived in the staging buffer until now
       __syncwarp();
       fence_proxy_async_smem();
+      hn = unpack_header<L, T>(hB, lpB);
       if (lane == 0 && hn.lp >= 0) issue_tma<L, T, P>(p, hn, buf, bar, policy);
     }
     uint8_t st = S.st;
     if (st == 0 && (S.pos0 < 4 || S.pos1 < 4)) st = 2;
     if (lane == 0) write_main(p, h, st, S.px, S.py, S.viol, S.wu);
+#ifdef LP2D_PROFILE_TIMELINE
+    if (lane == 0) {  // debug: per LP (start ns low 40 bits << 24 | duration ns), SM id
+      uint64_t tl_t1;
+      uint32_t smid;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_t1));
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      const uint64_t d = min(tl_t1 - tl_t0, (uint64_t)0xffffff);
+      p.wu[h.lp] = ((tl_t0 & 0xffffffffffull) << 24) | d;
+      p.viol[h.lp] = (smid << 16) | (uint32_t)(blockIdx.x * W + wic) % 65536u;
+    }
+#endif
     // pair export: lanes 0/1 request perm[pos-4] now, store one LP later
     pend_lp = h.lp;
     pend_pos = lane == 0 ? S.pos0 : S.pos1;
