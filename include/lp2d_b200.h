@@ -141,6 +141,11 @@ int lp2dgpu_shuffle_device(int64_t n, const int32_t* m, const int64_t* offset,
 /* Number of visible CUDA devices (0 when none). */
 int lp2dgpu_device_count(void);
 
+/* Number of kernels this library has enqueued so far (all devices, all
+ * calls; monotonic). A solve of a uniform batch is one launch; a mixed batch
+ * adds the two binning kernels and one launch per non-empty size class. */
+uint64_t lp2dgpu_kernel_launches(void);
+
 /* Thread-local message for the last non-zero return code. */
 const char* lp2dgpu_last_error(void);
 

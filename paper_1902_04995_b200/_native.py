@@ -85,6 +85,7 @@ EXPORTS = (
     "lp2dgpu_partition",
     "lp2dgpu_shuffle_device",
     "lp2dgpu_device_count",
+    "lp2dgpu_kernel_launches",
     "lp2dgpu_last_error",
     "lp2dgpu_version",
     "lp2dgen_derive_seed",
@@ -128,6 +129,7 @@ def lib():
                                          C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
     L.lp2dgpu_shuffle_device.restype = C.c_int
     L.lp2dgpu_device_count.restype = C.c_int
+    L.lp2dgpu_kernel_launches.restype = C.c_uint64
     L.lp2dgpu_last_error.restype = C.c_char_p
     L.lp2dgpu_version.restype = C.c_char_p
     L.lp2dgen_derive_seed.argtypes = [C.c_uint64, C.c_uint64]

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -37,6 +38,10 @@ int fail(int code, const std::string& msg) {
     }                                                                      \
   } while (0)
 
+// Kernels enqueued by this library (all devices), lp2dgpu_kernel_launches().
+std::atomic<uint64_t> g_launches{0};
+inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 constexpr int kCounterSlots = 4096;
 
 // Per-device state: ticket counters (self-resetting, round-robin slots) and a
@@ -54,6 +59,10 @@ struct DeviceState {
   std::mutex fork_mu;
   cudaStream_t cls_stream[16] = {};
   cudaEvent_t cls_event[17] = {};
+  // Stream-ordered workspace pool (binning lists) that keeps its memory:
+  // the default pool returns freed memory at every synchronisation, making
+  // the next allocation remap it (milliseconds, randomly).
+  cudaMemPool_t pool = nullptr;
 };
 
 DeviceState g_dev[64];
@@ -77,6 +86,13 @@ int ensure_device(int dev) {
   CUDA_TRY(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
   for (auto& cs : d.cls_stream) CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   for (auto& ce : d.cls_event) CUDA_TRY(cudaEventCreateWithFlags(&ce, cudaEventDisableTiming));
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  CUDA_TRY(cudaMemPoolCreate(&d.pool, &props));
+  uint64_t keep = UINT64_MAX;
+  CUDA_TRY(cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &keep));
   CUDA_TRY(cudaDeviceSynchronize());
   d.init = true;
   return 0;
@@ -126,6 +142,41 @@ int launch_warp_kernel(KParams kp, int dev, cudaStream_t stream) {
   kp.total_warps = grid * kWarpsPerCta;
   kp.counter = take_counter(dev);
   kern<<<grid, kWarpsPerCta * 32, L::kSmem, stream>>>(kp);
+  note_launch();
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// Tiny class (m <= 28): lane-per-LP kernel (k_solve_lanes), 32 LPs per warp.
+// LP2D_B200_TINY=warp selects the warp-per-LP kernel instead (A/B switch).
+bool tiny_uses_lanes() {
+  static const bool lanes = [] {
+    const char* e = std::getenv("LP2D_B200_TINY");
+    return !(e && std::strcmp(e, "warp") == 0);
+  }();
+  return lanes;
+}
+
+template <typename T, typename P>
+int launch_lane_kernel(KParams kp, int dev, cudaStream_t stream) {
+  auto kern = k_solve_lanes<T, P>;
+  constexpr size_t smem = LaneTile<T>::kSmem;
+  static int blocks_per_sm[64] = {0};
+  if (!blocks_per_sm[dev]) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int b = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kLaneWarps * 32, smem));
+    if (b < 1) return fail(LP2D_ERR_CUDA, "lane kernel does not fit on an SM");
+    blocks_per_sm[dev] = b;
+  }
+  const int64_t groups = (kp.n_list + 31) / 32;
+  const int64_t want = (groups + kLaneWarps - 1) / kLaneWarps;
+  const int64_t maxb = (int64_t)blocks_per_sm[dev] * g_dev[dev].sm_count;
+  const int grid = (int)std::max<int64_t>(1, std::min(want, maxb));
+  kp.total_warps = grid * kLaneWarps;
+  kp.counter = take_counter(dev);
+  kern<<<grid, kLaneWarps * 32, smem, stream>>>(kp);
+  note_launch();
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -162,6 +213,7 @@ int launch_global_kernel(KParams kp, int dev, cudaStream_t stream) {
   kp.total_warps = grid * kWarpsPerCta;
   kp.counter = take_counter(dev);
   kern<<<grid, kWarpsPerCta * 32, 0, stream>>>(kp);
+  note_launch();
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -187,6 +239,7 @@ int launch_cta_kernel(KParams kp, int64_t max_m, int dev, cudaStream_t stream) {
   kp.total_warps = grid;
   kp.counter = take_counter(dev);
   kern<<<grid, kCtaThreads, smem, stream>>>(kp, (int32_t)cap);
+  note_launch();
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -195,7 +248,9 @@ template <typename T, typename P>
 int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t max_m) {
   if (cls >= n_reg_classes<T>()) return launch_cta_kernel<T, P>(kp, max_m, dev, s);
   switch (kSlotClasses[cls]) {
-    case 1: return launch_warp_kernel<T, P, 1>(kp, dev, s);
+    case 1:
+      if (tiny_uses_lanes()) return launch_lane_kernel<T, P>(kp, dev, s);
+      return launch_warp_kernel<T, P, 1>(kp, dev, s);
     case 2: return launch_warp_kernel<T, P, 2>(kp, dev, s);
     case 3: return launch_warp_kernel<T, P, 3>(kp, dev, s);
     case 5: return launch_warp_kernel<T, P, 5>(kp, dev, s);
@@ -221,25 +276,50 @@ int launch_balanced(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStrea
   BinSpec spec{};
   spec.nreg = n_reg_classes<T>();
   for (int c = 0; c < spec.nreg; ++c) spec.slots[c] = kSlotClasses[c];
-  const size_t ws_bytes = 2 * 16 * sizeof(int32_t) + sizeof(int32_t) * (size_t)kp.n_list;
+  // The lane kernel's class is split by m, so its LP list comes out sorted
+  // by m and a warp's 32 LPs have similar sizes (its sweep runs to the
+  // largest of them).
+  static const bool sort_tiny = !(std::getenv("LP2D_B200_SORT") && std::getenv("LP2D_B200_SORT")[0] == '0');
+  spec.lane_bins = tiny_uses_lanes() && sort_tiny ? kLaneMaxM + 1 : 0;
+  auto bin_range = [&](int c, int& lo, int& hi) {
+    if (spec.lane_bins == 0) {
+      lo = c;
+      hi = c + 1;
+    } else if (c == 0) {
+      lo = 0;
+      hi = spec.lane_bins;
+    } else {
+      lo = hi = c + spec.lane_bins - 1;
+      ++hi;
+    }
+  };
+  const size_t ws_bytes = 2 * kMaxBins * sizeof(int32_t) + sizeof(int32_t) * (size_t)kp.n_list;
   void* ws = nullptr;
-  CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, s));
+  CUDA_TRY(cudaMallocFromPoolAsync(&ws, ws_bytes, g_dev[dev].pool, s));
   int32_t* counts = static_cast<int32_t*>(ws);
-  int32_t* cursors = counts + 16;
-  int32_t* list = counts + 32;
-  CUDA_TRY(cudaMemsetAsync(counts, 0, 2 * 16 * sizeof(int32_t), s));
+  int32_t* cursors = counts + kMaxBins;
+  int32_t* list = counts + 2 * kMaxBins;
+  CUDA_TRY(cudaMemsetAsync(counts, 0, 2 * kMaxBins * sizeof(int32_t), s));
   const int threads = 256;
   const int grid = (int)std::min<int64_t>((kp.n_list + threads - 1) / threads,
                                           (int64_t)g_dev[dev].sm_count * 8);
   k_bin_count<<<grid, threads, 0, s>>>(kp.n_list, kp.m, spec, counts);
+  note_launch();
   k_bin_scatter<<<grid, threads, 0, s>>>(kp.n_list, kp.m, spec, counts, cursors, list);
+  note_launch();
   CUDA_TRY(cudaGetLastError());
   kp.list = list;
   kp.bin_counts = counts;
-  int32_t host_counts[16] = {0};
+  int32_t host_bins[kMaxBins] = {0};
   if (may_sync) {
-    CUDA_TRY(cudaMemcpyAsync(host_counts, counts, sizeof(host_counts), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(host_bins, counts, sizeof(host_bins), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  int64_t host_counts[16] = {0};
+  for (int c = 0; c <= spec.nreg; ++c) {
+    int lo, hi;
+    bin_range(c, lo, hi);
+    for (int q = lo; q < hi; ++q) host_counts[c] += host_bins[q];
   }
   int rc = 0;
   // One stream per class, forked from and joined back into s: a class's
@@ -252,7 +332,10 @@ int launch_balanced(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStrea
     for (int c = cmax; c >= cmin && rc == 0; --c) {
       if (may_sync && host_counts[c] == 0) continue;
       KParams kc = kp;
-      kc.bin_class = c;
+      int lo, hi;
+      bin_range(c, lo, hi);
+      kc.bin_lo = lo;
+      kc.bin_hi = hi;
       if (may_sync) kc.n_list = host_counts[c];
       cudaStream_t cs = d.cls_stream[c];
       CUDA_TRY(cudaStreamWaitEvent(cs, d.cls_event[16], 0));
@@ -276,6 +359,7 @@ int launch_solve(const KParams& kp, int64_t min_m, int64_t max_m, int perm_bits,
       k_solve_naive<T, uint16_t><<<(unsigned)grid, threads, 0, s>>>(kp);
     else
       k_solve_naive<T, uint32_t><<<(unsigned)grid, threads, 0, s>>>(kp);
+    note_launch();
     CUDA_TRY(cudaGetLastError());
     return 0;
   }
@@ -539,6 +623,7 @@ int lp2dgpu_shuffle_device(int64_t n, const int32_t* m, const int64_t* offset,
     k_shuffle<uint32_t><<<grid, threads, 0, s>>>(n, m, offset, seeds, static_cast<uint32_t*>(perm));
   else
     return fail(LP2D_ERR_ARG, "perm_bits must be 16 or 32");
+  note_launch();
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -550,6 +635,8 @@ int lp2dgpu_device_count(void) {
 }
 
 const char* lp2dgpu_last_error(void) { return g_err.c_str(); }
+
+uint64_t lp2dgpu_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* lp2dgpu_version(void) {
   return "lp2d_b200 0.1 (sm_100a; warp-register Seidel/RGB, TMA bulk prefetch)";

@@ -38,10 +38,11 @@ struct KParams {
   int64_t n_list;        // LPs this launch solves
   const int32_t* list;   // LP ids (nullptr: 0..n_list-1)
   // Size-class binning (mixed batches): when bin_counts is set, this launch
-  // solves class bin_class, i.e. the bin_counts[bin_class] ids stored in
-  // `list` after the ids of the lower classes (k_bin_* below).
+  // solves the ids of bins [bin_lo, bin_hi), stored in `list` after the ids
+  // of the lower bins (k_bin_* below). A class is one bin, except the tiny
+  // class of the lane kernel, which has one bin per m (ids sorted by m).
   const int32_t* bin_counts;
-  int32_t bin_class;
+  int32_t bin_lo, bin_hi;
   const int32_t* m;
   const int64_t* offset;
   const void* ax;
@@ -131,10 +132,11 @@ __device__ __forceinline__ void resolve_list(const KParams& p, const int32_t*& l
   list = p.list;
   n = p.n_list;
   if (p.bin_counts) {
-    int64_t base = 0;
-    for (int c = 0; c < p.bin_class; ++c) base += p.bin_counts[c];
+    int64_t base = 0, cnt = 0;
+    for (int c = 0; c < p.bin_lo; ++c) base += p.bin_counts[c];
+    for (int c = p.bin_lo; c < p.bin_hi; ++c) cnt += p.bin_counts[c];
     list = p.list + base;
-    n = p.bin_counts[p.bin_class];
+    n = cnt;
   }
 }
 
@@ -927,6 +929,173 @@ __global__ void __launch_bounds__(128) k_solve_naive(const KParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// Tiny LPs (m <= 28): one LP per LANE, 32 LPs per warp in lockstep — the
+// paper's RGB thread-per-LP layout, with the LPs staged in shared memory.
+// Each lane gathers its LP's constraints through the permutation into a
+// position-major tile (position k of lane l at [k*32 + l]: every lockstep
+// access is bank-conflict free), then the warp sweeps positions 4, 5, ...:
+// all lanes test position i of their own LP; the lanes that violated it run
+// the 1D fold over their positions 0..i-1 together (same trip count, so they
+// stay converged) and resolve. Per-event cost is a serial fold of <= 31 units
+// per lane instead of a warp-wide merge, which is what dominates tiny LPs.
+// The fold is wu_fold (fast division, per-LP parallel bound) with the exact
+// reference fold (wu_apply) redone for a lane when a unit is undecided — the
+// same exactness devices as the warp kernel. Box positions 0..3 are not
+// stored: their coefficients are constants.
+constexpr int kLaneWarps = 4;
+constexpr int kLaneMaxM = 28;
+
+template <typename T>
+struct LaneTile {
+  static constexpr int kPos = kLaneMaxM;  // stored positions 4..31
+  static constexpr size_t kWarpBytes = 3 * sizeof(T) * kPos * 32;
+  static constexpr size_t kSmem = kLaneWarps * kWarpBytes;
+};
+
+template <typename T>
+__device__ __forceinline__ void box_unit(int k, T M, T& bx, T& by, T& bb) {
+  bx = k == 0 ? T(1) : (k == 1 ? T(-1) : T(0));  // serial.hpp:47-52
+  by = k == 2 ? T(1) : (k == 3 ? T(-1) : T(0));
+  bb = M;
+}
+
+template <typename T, typename P>
+__global__ void __launch_bounds__(kLaneWarps * 32) k_solve_lanes(const KParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wic = threadIdx.x >> 5;
+  constexpr int NP = LaneTile<T>::kPos;
+  T* sx = reinterpret_cast<T*>(smem + wic * LaneTile<T>::kWarpBytes);
+  T* sy = sx + NP * 32;
+  T* sb = sy + NP * 32;
+  // user constraint at considered position k (>= 4) of this lane's LP
+  auto at = [&](int k) { return (k - 4) * 32 + lane; };
+  const int32_t* list;
+  int64_t n_list;
+  resolve_list(p, list, n_list);
+  const T eps_par = Eps<T>::par(p);
+  const T eps_feas = Eps<T>::feas(p);
+  const T eps_hi = Eps<T>::hi(p);
+  const int64_t groups = (n_list + 31) / 32;
+  const int64_t TW = p.total_warps;
+  int64_t g = (int64_t)blockIdx.x * kLaneWarps + wic;
+  while (g < groups) {
+    // next group's ticket now; consumed after this group (one group ahead)
+    const uint32_t ticket = atomic_add_if(p.counter, lane == 0);
+    const int64_t j = g * 32 + lane;
+    Header<T> h;
+    h.lp = j < n_list ? (list ? (int64_t)list[j] : j) : -1;
+    const bool live = h.lp >= 0;
+    h.m = live ? p.m[h.lp] : 0;
+    h.off = live ? p.offset[h.lp] : 0;
+    h.ok = h.m >= 0 && h.m <= kLaneMaxM;
+    h.cx = live ? static_cast<const T*>(p.c)[2 * h.lp] : T(0);
+    h.cy = live ? static_cast<const T*>(p.c)[2 * h.lp + 1] : T(0);
+    h.M = live ? static_cast<const T*>(p.bound_m)[h.lp] : T(0);
+    const int mj = live && h.ok ? h.m : 0;
+    // ---- gather through the permutation (serial.hpp:28-32 insertion order)
+    const T* gx = static_cast<const T*>(p.ax) + h.off;
+    const T* gy = static_cast<const T*>(p.ay) + h.off;
+    const T* gb = static_cast<const T*>(p.b) + h.off;
+    const P* gp = static_cast<const P*>(p.perm) + h.off;
+    const int mmax = __reduce_max_sync(kFull, (uint32_t)mj);
+    uint32_t pmax = 0;
+    decltype(float_bits(T(0))) sbits = float_bits(T(1));
+    for (int k0 = 0; k0 < mmax; k0 += 4) {
+      uint32_t o[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) o[u] = k0 + u < mj ? (uint32_t)gp[k0 + u] : 0u;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        pmax = max(pmax, o[u]);
+        const uint32_t oc = min(o[u], (uint32_t)max(mj - 1, 0));
+        if (k0 + u < mj) {
+          const T vx = gx[oc], vy = gy[oc], vb = gb[oc];
+          sbits = max(sbits, float_bits(fabs(vx) + fabs(vy)));
+          sx[at(4 + k0 + u)] = vx;
+          sy[at(4 + k0 + u)] = vy;
+          sb[at(4 + k0 + u)] = vb;
+        }
+      }
+    }
+    __syncwarp();
+    const bool bad = live && (!h.ok || (mj > 0 && pmax >= (uint32_t)mj));
+    const T m_all = float_from_bits<T>(sbits);
+    // Outside the fast path's proven range every unit is undecided, so the
+    // fold below is the exact reference fold for this lane.
+    const bool wild = !(m_all < Limits<T>::kBig) || !(fabs(h.M) < T(INFINITY));
+    const T lpbnd = wild ? T(INFINITY)
+                         : fmax(fmax(m_all, Limits<T>::kSmall) * eps_hi, FastDiv<T>::kDLo);
+    LPState<T> S;
+    lp_init(S, h);
+    S.st = bad ? 255 : 0;
+    const T cthr = eps_par * sqrt(h.cx * h.cx + h.cy * h.cy);
+    bool alive = live && !bad;
+    const int mpos = mj + 4;
+    const int pend = __reduce_max_sync(kFull, alive ? (uint32_t)mpos : 0u);
+    // ---- lockstep sweep (serial.hpp:168-186 per lane) ----------------------
+    for (int i = 4; i < pend; ++i) {
+      const bool v = alive && i < mpos &&
+                     !satisfied(sx[at(i)], sy[at(i)], sb[at(i)], S.px, S.py, eps_feas);
+      if (!__any_sync(kFull, v)) continue;
+      if (v) {
+        S.viol += 1;
+        S.wu += (uint32_t)i;
+        const Line<T> l = boundary_of(sx[at(i)], sy[at(i)], sb[at(i)]);
+        Acc<T> acc;
+        acc.uL = -T(INFINITY);
+        acc.uR = T(INFINITY);
+        acc.oL = acc.oR = acc.par = kNone;
+        bool rare = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          T bx, by, bb;
+          box_unit(k, h.M, bx, by, bb);
+          wu_fold(bx, by, bb, l, lpbnd, (uint32_t)k, true, acc, rare);
+        }
+#pragma unroll 4
+        for (int k = 4; k < i; ++k)
+          wu_fold(sx[at(k)], sy[at(k)], sb[at(k)], l, lpbnd, (uint32_t)k, true, acc, rare);
+        if (rare) {  // exact reference fold for this lane (rare)
+          acc.uL = -T(INFINITY);
+          acc.uR = T(INFINITY);
+          acc.oL = acc.oR = acc.par = kNone;
+          for (int k = 0; k < 4; ++k) {
+            T bx, by, bb;
+            box_unit(k, h.M, bx, by, bb);
+            wu_apply(bx, by, bb, l, eps_par, eps_feas, eps_hi, (uint32_t)k, acc);
+          }
+          for (int k = 4; k < i; ++k)
+            wu_apply(sx[at(k)], sy[at(k)], sb[at(k)], l, eps_par, eps_feas, eps_hi,
+                     (uint32_t)k, acc);
+        }
+        Merged<T> mg;
+        mg.uL = acc.uL;
+        mg.uR = acc.uR;
+        mg.oL = acc.oL;
+        mg.oR = acc.oR;
+        mg.par = acc.par;
+        if (!resolve_merged(S, mg, l, (uint32_t)i, h, cthr, eps_feas)) alive = false;
+      }
+    }
+    if (live) {
+      uint8_t st = S.st;
+      if (st == 0 && (S.pos0 < 4 || S.pos1 < 4)) st = 2;
+      write_result<T, P>(p, h, st, S.px, S.py, S.pos0, S.pos1, S.viol, S.wu);
+    }
+    __syncwarp();  // the tile is rewritten by the next group
+    g = (int64_t)__shfl_sync(kFull, ticket, 0) + TW;
+  }
+  if (lane == 0) {
+    __threadfence();
+    const uint32_t t = atomicAdd(p.counter + 1, 1u);
+    if (t == (uint32_t)p.total_warps - 1) {
+      p.counter[0] = 0;
+      p.counter[1] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Large LPs: one CTA (kCtaThreads threads) per LP. The LP is gathered once
 // from global memory through its permutation into shared memory in insertion
 // order (positions 0..3 = box), then
@@ -1221,42 +1390,59 @@ __device__ __forceinline__ int size_class(int32_t m, const int32_t* slots, int n
   return nreg;
 }
 
+constexpr int kMaxBins = 64;
+
 struct BinSpec {
   int32_t slots[8];
   int32_t nreg;
+  int32_t lane_bins;  // > 0: class 0 is split into one bin per m in [0, lane_bins)
 };
 
+// Bin of an LP: class 0 -> bin m (lane kernel) or 0; class c -> c + lane_bins - 1.
+__device__ __forceinline__ int bin_of(int32_t m, const BinSpec& spec) {
+  const int c = size_class(m, spec.slots, spec.nreg);
+  if (spec.lane_bins == 0) return c;
+  if (c == 0) return min(max(m, 0), spec.lane_bins - 1);
+  return c + spec.lane_bins - 1;
+}
+
 __global__ void k_bin_count(int64_t n, const int32_t* m, BinSpec spec, int32_t* counts) {
-  __shared__ int32_t local[9];
-  if (threadIdx.x < 9) local[threadIdx.x] = 0;
+  __shared__ int32_t local[kMaxBins];
+  for (int i = threadIdx.x; i < kMaxBins; i += blockDim.x) local[i] = 0;
   __syncthreads();
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&local[size_class(m[j], spec.slots, spec.nreg)], 1);
+    atomicAdd(&local[bin_of(m[j], spec)], 1);
   __syncthreads();
-  if (threadIdx.x <= spec.nreg && local[threadIdx.x]) atomicAdd(&counts[threadIdx.x], local[threadIdx.x]);
+  for (int i = threadIdx.x; i < kMaxBins; i += blockDim.x)
+    if (local[i]) atomicAdd(&counts[i], local[i]);
 }
 
 __global__ void k_bin_scatter(int64_t n, const int32_t* m, BinSpec spec, const int32_t* counts,
                               int32_t* cursors, int32_t* list) {
-  // Warp-aggregated slot reservation: one atomic per (warp, class) instead of
-  // one per LP on the same address.
+  // Bin bases once per block; then warp-aggregated slot reservation: one
+  // atomic per (warp, bin) instead of one per LP on the same address.
+  __shared__ int32_t base[kMaxBins];
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    for (int q = 0; q < kMaxBins; ++q) {
+      base[q] = acc;
+      acc += counts[q];
+    }
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < n; j0 += stride) {
     const int64_t j = j0 + threadIdx.x;
     const bool in = j < n;
-    const int c = in ? size_class(m[j], spec.slots, spec.nreg) : 15;
+    const int c = in ? bin_of(m[j], spec) : kMaxBins - 1;
     const uint32_t peers = __match_any_sync(kFull, c);
     const int leader = __ffs(peers) - 1;
     int32_t slot = 0;
     if (lane == leader && in) slot = atomicAdd(&cursors[c], __popc(peers));
     slot = __shfl_sync(kFull, slot, leader) + __popc(peers & ((1u << lane) - 1u));
-    if (in) {
-      int32_t base = 0;
-      for (int q = 0; q < c; ++q) base += counts[q];
-      list[base + slot] = (int32_t)j;
-    }
+    if (in) list[base[c] + slot] = (int32_t)j;
   }
 }
 

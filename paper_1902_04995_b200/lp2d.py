@@ -156,6 +156,11 @@ def shuffle(m: int, seed: int) -> Permutation:
     return Permutation(out)
 
 
+def kernel_launches() -> int:
+    """Kernels the native library has enqueued so far (monotonic counter)."""
+    return int(N.lib().lp2dgpu_kernel_launches())
+
+
 def pack_offsets(m: np.ndarray) -> np.ndarray:
     """Element offsets satisfying the C-ABI layout contract (8-aligned)."""
     m = np.ascontiguousarray(m, dtype=np.int32)

@@ -26,7 +26,8 @@ def assert_same_as_oracle(r, o, O, what=""):
     feas = o["status"] != O.INFEASIBLE
     for k in ("x", "y", "value"):
         g = getattr(r, k)[feas].astype(np.float64)
-        assert np.array_equal(g, o[k][feas]), f"{what}: {k} differs"
+        # (NaN == NaN here: overflowing inputs give NaN in both)
+        assert np.array_equal(g, o[k][feas], equal_nan=True), f"{what}: {k} differs"
     assert np.array_equal(r.violation_events.astype(np.uint64), o["violation_events"]), what
     assert np.array_equal(r.work_units, o["work_units"]), what
 
@@ -178,6 +179,46 @@ def test_wild_magnitudes_take_the_exact_path(P, O):
     assert_same_as_oracle(P.solve_packed(pb), O.solve_batch(pb), O, "wild")
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_tiny_lps_lane_kernel(P, O, dt):
+    """m <= 28 runs one LP per lane (k_solve_lanes): all generator kinds,
+    every size 0..28, wild magnitudes (exact fold per lane), an invalid
+    permutation, alone (uniform launch) and mixed with larger LPs (binned,
+    lane class sorted by m), host and device mode."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    m = rng.integers(0, 29, 3000).astype(np.int32)
+    kind = rng.choice([P.GenKind.feasible_random, P.GenKind.infeasible,
+                       P.GenKind.unbounded_random], 3000).astype(np.uint8)
+    kind[m < 1] = P.GenKind.feasible_random  # (infeasible needs m >= 1)
+    pb = P.PackedBatch.generate(m, 31, kind=kind).astype(dt)
+    e = int(pb.offset[100])
+    pb.ax[:e] *= dt(1e20) if dt == np.float32 else dt(1e160)
+    pb.b[int(pb.offset[200]):int(pb.offset[260])] *= dt(1e-30)
+    pb.ay[int(pb.offset[300]):int(pb.offset[340])] = 0.0
+    o = O.solve_batch(pb)
+    r = P.solve_packed(pb)
+    assert_same_as_oracle(r, o, O, "tiny")
+    bad = pb.subset(0, 64)
+    j = int(np.nonzero(bad.m > 3)[0][0])
+    bad.perm = bad.perm.copy()
+    bad.perm[int(bad.offset[j]) + 1] = 1000
+    rb = P.solve_packed(bad)
+    assert rb.status[j] == 255 and (np.delete(rb.status, j) != 255).all()
+    # mixed with larger LPs: the binned path with per-m sub-bins
+    mix = P.PackedBatch.generate(np.concatenate([m[:1500], rng.integers(29, 400, 500)]).astype(np.int32),
+                                 32).astype(dt)
+    om = O.solve_batch(mix)
+    assert_same_as_oracle(P.solve_packed(mix), om, O, "tiny+mixed")
+    db = P.DeviceBatch(mix)
+    out = db.empty_result()
+    P.solve_device(db, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.status.cpu().numpy().astype(np.int32), om["status"])
+    assert np.array_equal(out.work_units.cpu().numpy(), om["work_units"])
+
+
 def test_batch_api_matches_serial_semantics(P, O):
     """test_batch.cpp:55-74: both schedulers == serial, stats equal."""
     base = P.gen(128, 77)
@@ -210,6 +251,21 @@ def test_device_mode_matches_host_mode(P):
         P.solve_device(db, out)
     torch.cuda.synchronize()
     assert np.array_equal(out.value.cpu().numpy(), host.value)
+
+
+def test_kernel_launch_counter(P):
+    import torch
+
+    uni = P.DeviceBatch(P.PackedBatch.generate(np.full(512, 200, np.int32), 3).astype(np.float32))
+    mixed = P.DeviceBatch(P.PackedBatch.generate(np.array([8, 40, 100, 700, 3000], np.int32)
+                                                 .repeat(64), 3).astype(np.float32))
+    for db, lo, hi in ((uni, 1, 1), (mixed, 3, 2 + 8)):
+        out = db.empty_result()
+        k0 = P.kernel_launches()
+        P.solve_device(db, out)
+        k = P.kernel_launches() - k0
+        torch.cuda.synchronize()
+        assert lo <= k <= hi, k
 
 
 def test_device_shuffle_matches_host(P):
