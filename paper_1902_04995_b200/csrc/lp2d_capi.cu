@@ -157,10 +157,10 @@ bool tiny_uses_lanes() {
   return lanes;
 }
 
-template <typename T, typename P>
+template <typename T, typename P, int MAXM = kLaneMaxM>
 int launch_lane_kernel(KParams kp, int dev, cudaStream_t stream) {
-  auto kern = k_solve_lanes<T, P>;
-  constexpr size_t smem = LaneTile<T>::kSmem;
+  auto kern = k_solve_lanes<T, P, MAXM>;
+  constexpr size_t smem = LaneTile<T, MAXM>::kSmem;
   static int blocks_per_sm[64] = {0};
   if (!blocks_per_sm[dev]) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -218,30 +218,40 @@ int launch_global_kernel(KParams kp, int dev, cudaStream_t stream) {
   return 0;
 }
 
-// Large class: CTA per LP with the LP in shared memory (k_solve_cta); the
-// smem capacity covers the class's largest LP up to ~200 KB, bigger LPs are
-// solved by the CTA's warp 0 from global memory.
-template <typename T, typename P>
-int launch_cta_kernel(KParams kp, int64_t max_m, int dev, cudaStream_t stream) {
-  auto kern = k_solve_cta<T, P>;
-  const size_t head = (sizeof(CtaShared<T>) + 127) & ~size_t(127);
-  const size_t max_bytes = 200 * 1024;
-  int64_t cap = ((max_m + 4 + 255) / 256) * 256;
-  const int64_t cap_max = (int64_t)((max_bytes - head) / (3 * sizeof(T))) & ~int64_t(255);
-  cap = std::min(cap, cap_max);
-  const size_t smem = head + 3 * sizeof(T) * (size_t)cap;
+// Large class: CTA per LP with the LP resident in shared memory
+// (k_solve_cta). Capacity = the class's largest LP, bounded by the opt-in
+// shared memory per block; bigger LPs are solved by the CTA's warp 0 from
+// global memory. 512 threads when one CTA fills the SM, else 256.
+template <typename T, typename P, int THREADS>
+int launch_cta_t(KParams kp, int64_t cap, size_t smem, int dev, cudaStream_t stream) {
+  auto kern = k_solve_cta<T, P, THREADS>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int b = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kCtaThreads, smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, THREADS, smem));
   b = std::max(b, 1);
   const int64_t maxb = (int64_t)b * g_dev[dev].sm_count;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kp.n_list, maxb));
   kp.total_warps = grid;
   kp.counter = take_counter(dev);
-  kern<<<grid, kCtaThreads, smem, stream>>>(kp, (int32_t)cap);
+  kern<<<grid, THREADS, smem, stream>>>(kp, (int32_t)cap);
   note_launch();
   CUDA_TRY(cudaGetLastError());
   return 0;
+}
+
+template <typename T, typename P>
+int launch_cta_kernel(KParams kp, int64_t max_m, int dev, cudaStream_t stream) {
+  int optin = 0, per_sm = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  int64_t cap = std::max<int64_t>(16, ((max_m + 15) / 16) * 16);
+  while (cap > 16 && CtaBuffers<T, P>::bytes(cap) > (size_t)optin) cap -= 16;
+  const size_t smem = CtaBuffers<T, P>::bytes(cap);
+  // 16 warps per SM, split over as many CTAs (LPs) as shared memory allows
+  const int ctas = (int)std::max<size_t>(1, (size_t)per_sm / (smem + 1024));
+  if (ctas >= 4) return launch_cta_t<T, P, 128>(kp, cap, smem, dev, stream);
+  if (ctas >= 2) return launch_cta_t<T, P, 256>(kp, cap, smem, dev, stream);
+  return launch_cta_t<T, P, 512>(kp, cap, smem, dev, stream);
 }
 
 template <typename T, typename P>
@@ -281,16 +291,21 @@ int launch_balanced(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStrea
   // largest of them).
   static const bool sort_tiny = !(std::getenv("LP2D_B200_SORT") && std::getenv("LP2D_B200_SORT")[0] == '0');
   spec.lane_bins = tiny_uses_lanes() && sort_tiny ? kLaneMaxM + 1 : 0;
+  // The large class is split by m (256 per bin, largest first): LPT order.
+  spec.cta_bins = 64;
+  spec.cta_lo = 32 * kSlotClasses[spec.nreg - 1] - 3;
+  spec.cta_width = 256;
   auto bin_range = [&](int c, int& lo, int& hi) {
-    if (spec.lane_bins == 0) {
-      lo = c;
-      hi = c + 1;
-    } else if (c == 0) {
+    const int b0 = spec.lane_bins ? spec.lane_bins : 1;
+    if (c == 0) {
       lo = 0;
-      hi = spec.lane_bins;
+      hi = b0;
+    } else if (c < spec.nreg) {
+      lo = b0 + c - 1;
+      hi = lo + 1;
     } else {
-      lo = hi = c + spec.lane_bins - 1;
-      ++hi;
+      lo = b0 + spec.nreg - 1;
+      hi = lo + spec.cta_bins;
     }
   };
   const size_t ws_bytes = 2 * kMaxBins * sizeof(int32_t) + sizeof(int32_t) * (size_t)kp.n_list;

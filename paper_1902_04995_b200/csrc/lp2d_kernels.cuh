@@ -929,26 +929,29 @@ __global__ void __launch_bounds__(128) k_solve_naive(const KParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// Tiny LPs (m <= 28): one LP per LANE, 32 LPs per warp in lockstep — the
-// paper's RGB thread-per-LP layout, with the LPs staged in shared memory.
-// Each lane gathers its LP's constraints through the permutation into a
-// position-major tile (position k of lane l at [k*32 + l]: every lockstep
-// access is bank-conflict free), then the warp sweeps positions 4, 5, ...:
-// all lanes test position i of their own LP; the lanes that violated it run
-// the 1D fold over their positions 0..i-1 together (same trip count, so they
-// stay converged) and resolve. Per-event cost is a serial fold of <= 31 units
-// per lane instead of a warp-wide merge, which is what dominates tiny LPs.
-// The fold is wu_fold (fast division, per-LP parallel bound) with the exact
-// reference fold (wu_apply) redone for a lane when a unit is undecided — the
-// same exactness devices as the warp kernel. Box positions 0..3 are not
-// stored: their coefficients are constants.
+// Small LPs (m <= MAXM): one LP per LANE, 32 LPs per warp in lockstep — the
+// paper's RGB layout (thread per LP, block-wide work-unit deal). Each lane
+// gathers its LP's constraints through the permutation into a shared tile
+// (element (position k, lane l) at [(k-4)*33 + l]: conflict-free both for
+// all lanes reading their own position k and for all lanes reading one
+// lane's positions). The warp sweeps positions 4, 5, ...: every lane tests
+// position i of its own LP (one test per lane per step). The lanes that
+// violated position i need a 1D fold over their positions 0..i-1; per step
+// the warp picks the cheaper deal:
+//   * lane-serial: each violated lane folds its own i units (cost ~ i);
+//   * pooled: for each violated lane in turn the whole warp folds that LP's
+//     i units (ceil(i/32) per lane) and merges them with REDUX — the balanced
+//     deal of batch.hpp:219-240 with the warp as the block (cost ~ #violated).
+// Both folds are wu_fold (fast division, per-LP parallel bound) with the
+// exact reference fold (wu_apply) redone when a unit is undecided, as in the
+// warp kernel. Box positions 0..3 are constants, not stored.
 constexpr int kLaneWarps = 4;
 constexpr int kLaneMaxM = 28;
 
-template <typename T>
+template <typename T, int MAXM>
 struct LaneTile {
-  static constexpr int kPos = kLaneMaxM;  // stored positions 4..31
-  static constexpr size_t kWarpBytes = 3 * sizeof(T) * kPos * 32;
+  static constexpr int kStride = 33;
+  static constexpr size_t kWarpBytes = 3 * sizeof(T) * MAXM * kStride;
   static constexpr size_t kSmem = kLaneWarps * kWarpBytes;
 };
 
@@ -959,16 +962,27 @@ __device__ __forceinline__ void box_unit(int k, T M, T& bx, T& by, T& bb) {
   bb = M;
 }
 
-template <typename T, typename P>
-__global__ void __launch_bounds__(kLaneWarps * 32) k_solve_lanes(const KParams p) {
+template <typename T>
+__device__ __forceinline__ Line<T> shfl_line(const Line<T>& l, int src) {
+  Line<T> r;
+  r.ox = __shfl_sync(kFull, l.ox, src);
+  r.oy = __shfl_sync(kFull, l.oy, src);
+  r.dx = __shfl_sync(kFull, l.dx, src);
+  r.dy = __shfl_sync(kFull, l.dy, src);
+  return r;
+}
+
+template <typename T, typename P, int MAXM>
+__global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
+  using LT = LaneTile<T, MAXM>;
+  constexpr int ST = LT::kStride;
   const int lane = threadIdx.x & 31, wic = threadIdx.x >> 5;
-  constexpr int NP = LaneTile<T>::kPos;
-  T* sx = reinterpret_cast<T*>(smem + wic * LaneTile<T>::kWarpBytes);
-  T* sy = sx + NP * 32;
-  T* sb = sy + NP * 32;
-  // user constraint at considered position k (>= 4) of this lane's LP
-  auto at = [&](int k) { return (k - 4) * 32 + lane; };
+  T* sx = reinterpret_cast<T*>(smem + wic * LT::kWarpBytes);
+  T* sy = sx + MAXM * ST;
+  T* sb = sy + MAXM * ST;
+  // user constraint at considered position k (>= 4) of lane c's LP
+  auto at = [&](int k, int c) { return (k - 4) * ST + c; };
   const int32_t* list;
   int64_t n_list;
   resolve_list(p, list, n_list);
@@ -987,7 +1001,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32) k_solve_lanes(const KParams p
     const bool live = h.lp >= 0;
     h.m = live ? p.m[h.lp] : 0;
     h.off = live ? p.offset[h.lp] : 0;
-    h.ok = h.m >= 0 && h.m <= kLaneMaxM;
+    h.ok = h.m >= 0 && h.m <= MAXM;
     h.cx = live ? static_cast<const T*>(p.c)[2 * h.lp] : T(0);
     h.cy = live ? static_cast<const T*>(p.c)[2 * h.lp + 1] : T(0);
     h.M = live ? static_cast<const T*>(p.bound_m)[h.lp] : T(0);
@@ -1011,9 +1025,9 @@ __global__ void __launch_bounds__(kLaneWarps * 32) k_solve_lanes(const KParams p
         if (k0 + u < mj) {
           const T vx = gx[oc], vy = gy[oc], vb = gb[oc];
           sbits = max(sbits, float_bits(fabs(vx) + fabs(vy)));
-          sx[at(4 + k0 + u)] = vx;
-          sy[at(4 + k0 + u)] = vy;
-          sb[at(4 + k0 + u)] = vb;
+          sx[at(4 + k0 + u, lane)] = vx;
+          sy[at(4 + k0 + u, lane)] = vy;
+          sb[at(4 + k0 + u, lane)] = vb;
         }
       }
     }
@@ -1021,7 +1035,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32) k_solve_lanes(const KParams p
     const bool bad = live && (!h.ok || (mj > 0 && pmax >= (uint32_t)mj));
     const T m_all = float_from_bits<T>(sbits);
     // Outside the fast path's proven range every unit is undecided, so the
-    // fold below is the exact reference fold for this lane.
+    // folds below are the exact reference fold for this LP.
     const bool wild = !(m_all < Limits<T>::kBig) || !(fabs(h.M) < T(INFINITY));
     const T lpbnd = wild ? T(INFINITY)
                          : fmax(fmax(m_all, Limits<T>::kSmall) * eps_hi, FastDiv<T>::kDLo);
@@ -1035,46 +1049,101 @@ __global__ void __launch_bounds__(kLaneWarps * 32) k_solve_lanes(const KParams p
     // ---- lockstep sweep (serial.hpp:168-186 per lane) ----------------------
     for (int i = 4; i < pend; ++i) {
       const bool v = alive && i < mpos &&
-                     !satisfied(sx[at(i)], sy[at(i)], sb[at(i)], S.px, S.py, eps_feas);
-      if (!__any_sync(kFull, v)) continue;
+                     !satisfied(sx[at(i, lane)], sy[at(i, lane)], sb[at(i, lane)], S.px, S.py,
+                                eps_feas);
+      uint32_t vm = __ballot_sync(kFull, v);
+      if (!vm) continue;
+      Line<T> l;
       if (v) {
         S.viol += 1;
         S.wu += (uint32_t)i;
-        const Line<T> l = boundary_of(sx[at(i)], sy[at(i)], sb[at(i)]);
-        Acc<T> acc;
-        acc.uL = -T(INFINITY);
-        acc.uR = T(INFINITY);
-        acc.oL = acc.oR = acc.par = kNone;
-        bool rare = false;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          T bx, by, bb;
-          box_unit(k, h.M, bx, by, bb);
-          wu_fold(bx, by, bb, l, lpbnd, (uint32_t)k, true, acc, rare);
-        }
-#pragma unroll 4
-        for (int k = 4; k < i; ++k)
-          wu_fold(sx[at(k)], sy[at(k)], sb[at(k)], l, lpbnd, (uint32_t)k, true, acc, rare);
-        if (rare) {  // exact reference fold for this lane (rare)
+        l = boundary_of(sx[at(i, lane)], sy[at(i, lane)], sb[at(i, lane)]);
+      }
+      const int nv = __popc(vm);
+      if (nv * (((i + 31) >> 5) * 26 + 64) >= i * 22) {
+        // ---- lane-serial folds ----------------------------------------------
+        if (v) {
+          Acc<T> acc;
           acc.uL = -T(INFINITY);
           acc.uR = T(INFINITY);
           acc.oL = acc.oR = acc.par = kNone;
+          bool rare = false;
+#pragma unroll
           for (int k = 0; k < 4; ++k) {
             T bx, by, bb;
             box_unit(k, h.M, bx, by, bb);
-            wu_apply(bx, by, bb, l, eps_par, eps_feas, eps_hi, (uint32_t)k, acc);
+            wu_fold(bx, by, bb, l, lpbnd, (uint32_t)k, true, acc, rare);
           }
+#pragma unroll 4
           for (int k = 4; k < i; ++k)
-            wu_apply(sx[at(k)], sy[at(k)], sb[at(k)], l, eps_par, eps_feas, eps_hi,
-                     (uint32_t)k, acc);
+            wu_fold(sx[at(k, lane)], sy[at(k, lane)], sb[at(k, lane)], l, lpbnd, (uint32_t)k,
+                    true, acc, rare);
+          if (rare) {  // exact reference fold for this lane (rare)
+            acc.uL = -T(INFINITY);
+            acc.uR = T(INFINITY);
+            acc.oL = acc.oR = acc.par = kNone;
+            for (int k = 0; k < 4; ++k) {
+              T bx, by, bb;
+              box_unit(k, h.M, bx, by, bb);
+              wu_apply(bx, by, bb, l, eps_par, eps_feas, eps_hi, (uint32_t)k, acc);
+            }
+            for (int k = 4; k < i; ++k)
+              wu_apply(sx[at(k, lane)], sy[at(k, lane)], sb[at(k, lane)], l, eps_par, eps_feas,
+                       eps_hi, (uint32_t)k, acc);
+          }
+          Merged<T> mg;
+          mg.uL = acc.uL;
+          mg.uR = acc.uR;
+          mg.oL = acc.oL;
+          mg.oR = acc.oR;
+          mg.par = acc.par;
+          if (!resolve_merged(S, mg, l, (uint32_t)i, h, cthr, eps_feas)) alive = false;
         }
-        Merged<T> mg;
-        mg.uL = acc.uL;
-        mg.uR = acc.uR;
-        mg.oL = acc.oL;
-        mg.oR = acc.oR;
-        mg.par = acc.par;
-        if (!resolve_merged(S, mg, l, (uint32_t)i, h, cthr, eps_feas)) alive = false;
+      } else {
+        // ---- pooled: the warp folds each violated LP in turn ----------------
+        while (vm) {
+          const int c = __ffs(vm) - 1;
+          vm &= vm - 1;
+          const Line<T> lc = shfl_line(l, c);
+          const T Mc = __shfl_sync(kFull, h.M, c);
+          const T bnd = __shfl_sync(kFull, lpbnd, c);
+          Acc<T> acc;
+          acc.uL = -T(INFINITY);
+          acc.uR = T(INFINITY);
+          acc.oL = acc.oR = acc.par = kNone;
+          bool rare = false;
+          for (int k = lane; k < i; k += 32) {
+            T x, y, bb;
+            if (k < 4) {
+              box_unit(k, Mc, x, y, bb);
+            } else {
+              x = sx[at(k, c)];
+              y = sy[at(k, c)];
+              bb = sb[at(k, c)];
+            }
+            wu_fold(x, y, bb, lc, bnd, (uint32_t)k, true, acc, rare);
+          }
+          const bool rare_any = __any_sync(kFull, rare);
+          if (rare_any) {  // exact reference fold, pooled the same way
+            acc.uL = -T(INFINITY);
+            acc.uR = T(INFINITY);
+            acc.oL = acc.oR = acc.par = kNone;
+            for (int k = lane; k < i; k += 32) {
+              T x, y, bb;
+              if (k < 4) {
+                box_unit(k, Mc, x, y, bb);
+              } else {
+                x = sx[at(k, c)];
+                y = sy[at(k, c)];
+                bb = sb[at(k, c)];
+              }
+              wu_apply(x, y, bb, lc, eps_par, eps_feas, eps_hi, (uint32_t)k, acc);
+            }
+          }
+          const Merged<T> mg = merge_lanes(acc, rare_any);
+          if (lane == c && !resolve_merged(S, mg, l, (uint32_t)i, h, cthr, eps_feas))
+            alive = false;
+        }
       }
     }
     if (live) {
@@ -1096,40 +1165,75 @@ __global__ void __launch_bounds__(kLaneWarps * 32) k_solve_lanes(const KParams p
 }
 
 // ---------------------------------------------------------------------------
-// Large LPs: one CTA (kCtaThreads threads) per LP. The LP is gathered once
-// from global memory through its permutation into shared memory in insertion
-// order (positions 0..3 = box), then
-//   * the violation test sweeps kCtaThreads positions per step (warp ballots
-//     combined through shared memory, first violated position wins);
+// Large LPs: one CTA (THREADS threads) per LP, the LP resident in shared
+// memory in its ORIGINAL order (ax, ay, b, perm: 14 B per constraint in fp32,
+// so two m = 8192 LPs fit an SM and one CTA's event latency hides behind the
+// other's work). Per LP:
+//   * warp 0 stages the raw segments with 1D bulk TMA (contiguous in HBM);
+//   * positions are read through the staged permutation (position k >= 4 is
+//     element perm[k-4]; 0..3 are the box constants);
+//   * the violation test sweeps THREADS positions per step (warp ballots
+//     through a double-buffered shared array: one barrier per step, first
+//     violated position found with one more ballot);
 //   * a violation's 1D re-solve deals the prefix round-robin over ALL threads
-//     of the CTA (the reference's balanced deal with the CTA as the block,
-//     batch.hpp:219-240), lanes fold branch-free (wu_fold), warps merge with
-//     REDUX and the 8 warp results are merged through shared memory;
+//     (the reference's balanced deal with the CTA as the block,
+//     batch.hpp:219-240), folded branch-free (wu_fold), merged with REDUX per
+//     warp and once more across the warps' results;
 //   * every thread resolves the event redundantly (identical inputs and
 //     operations), so the new optimum needs no broadcast.
-// LPs whose size exceeds the launch's shared-memory capacity, or whose
-// magnitudes leave the fast path's range, are solved by warp 0 with
+// Warp 0 keeps the next LP's ticket and header one LP ahead. The class's LPs
+// come sorted by decreasing m (LPT). LPs larger than the launch's capacity,
+// or outside the fast path's range, are solved by warp 0 with
 // solve_exact_global.
-constexpr int kCtaThreads = 128;
-constexpr int kCtaWarps = kCtaThreads / 32;
+constexpr int kCtaMaxWarps = 16;
 
 template <typename T>
 struct CtaShared {
-  T vL[kCtaWarps], vR[kCtaWarps];  // per-warp merged interval endpoints
-  int64_t lp_next;
-  uint32_t oL[kCtaWarps], oR[kCtaWarps], par[kCtaWarps];
-  uint32_t bal[kCtaWarps];         // per-warp violation ballots of a test step
-  uint32_t redk[kCtaWarps][3];     // per-warp pmax / |a| bound words
+  uint64_t bar;
+  Header<T> hdr;
+  uint32_t bal[2][kCtaMaxWarps];   // per-warp ballots, double-buffered by step
+  T vL[kCtaMaxWarps], vR[kCtaMaxWarps];  // per-warp merged interval endpoints
+  uint32_t oL[kCtaMaxWarps], oR[kCtaMaxWarps], par[kCtaMaxWarps];
+  uint32_t redk[kCtaMaxWarps][3];  // per-warp pmax / |a| bound words
 };
 
 template <typename T, typename P>
-__global__ void __launch_bounds__(kCtaThreads) k_solve_cta(const KParams p, int32_t cap_pos) {
+struct CtaBuffers {
+  static __host__ __device__ size_t head() { return (sizeof(CtaShared<T>) + 127) & ~size_t(127); }
+  static __host__ __device__ size_t bytes(int64_t cap) {
+    return head() + (3 * sizeof(T) + sizeof(P)) * (size_t)cap;
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ Header<T> unpack_header_cap(uint32_t w, int64_t lp, int64_t cap,
+                                                       bool& fits) {
+  constexpr int WT = sizeof(T) / 4;
+  Header<T> h;
+  h.lp = lp;
+  h.m = (int32_t)__shfl_sync(kFull, w, 0);
+  h.off = (int64_t)(((uint64_t)__shfl_sync(kFull, w, 2) << 32) | __shfl_sync(kFull, w, 1));
+  const int64_t o1 = (int64_t)(((uint64_t)__shfl_sync(kFull, w, 4) << 32) | __shfl_sync(kFull, w, 3));
+  h.cx = word_scalar<T>(w, 5);
+  h.cy = word_scalar<T>(w, 5 + WT);
+  h.M = word_scalar<T>(w, 5 + 2 * WT);
+  const int64_t cap8 = ((int64_t)h.m + 7) & ~int64_t(7);
+  h.ok = h.m >= 0 && (h.off & 7) == 0 && o1 - h.off >= cap8;
+  fits = h.ok && h.m <= cap;
+  return h;
+}
+
+template <typename T, typename P, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_solve_cta(const KParams p, int32_t cap) {
   static_assert(sizeof(T) == 4 || sizeof(T) == 8, "scalar");
+  constexpr int W = THREADS / 32;
+  static_assert(W <= kCtaMaxWarps, "warps per CTA");
   extern __shared__ __align__(128) unsigned char smem[];
   CtaShared<T>& sh = *reinterpret_cast<CtaShared<T>*>(smem);
-  T* pax = reinterpret_cast<T*>(smem + ((sizeof(CtaShared<T>) + 127) & ~size_t(127)));
-  T* pay = pax + cap_pos;
-  T* pb = pay + cap_pos;
+  T* rax = reinterpret_cast<T*>(smem + CtaBuffers<T, P>::head());
+  T* ray = rax + cap;
+  T* rb = ray + cap;
+  P* rperm = reinterpret_cast<P*>(rb + cap);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int32_t* list;
   int64_t n_list;
@@ -1137,67 +1241,71 @@ __global__ void __launch_bounds__(kCtaThreads) k_solve_cta(const KParams p, int3
   const T eps_par = Eps<T>::par(p);
   const T eps_feas = Eps<T>::feas(p);
   const T eps_hi = Eps<T>::hi(p);
-  int64_t j = blockIdx.x;
-  while (j < n_list) {
-    Header<T> h;
-    h.lp = list ? (int64_t)list[j] : j;
-    h.m = p.m[h.lp];
-    h.off = p.offset[h.lp];
-    h.ok = h.m >= 0;
-    h.cx = static_cast<const T*>(p.c)[2 * h.lp];
-    h.cy = static_cast<const T*>(p.c)[2 * h.lp + 1];
-    h.M = static_cast<const T*>(p.bound_m)[h.lp];
-    if (tid == 0) sh.lp_next = (int64_t)atomicAdd(p.counter, 1u) + gridDim.x;
-    const int mpos = h.m + 4;
-    const bool fits = h.ok && mpos <= cap_pos;
-    // ---- gather (global -> shared, insertion order) ----------------------
-    uint32_t pmax = 0;
-    decltype(float_bits(T(0))) sbits = float_bits(T(1));
-    const T* gax = static_cast<const T*>(p.ax) + h.off;
-    const T* gay = static_cast<const T*>(p.ay) + h.off;
-    const T* gb = static_cast<const T*>(p.b) + h.off;
-    const P* gperm = static_cast<const P*>(p.perm) + h.off;
-    if (fits) {
-      if (tid < 4) {
-        pax[tid] = tid == 0 ? T(1) : (tid == 1 ? T(-1) : T(0));
-        pay[tid] = tid == 2 ? T(1) : (tid == 3 ? T(-1) : T(0));
-        pb[tid] = h.M;
-      }
-      // Random gathers from L2/HBM: batches of 8 independent chains per
-      // thread keep enough loads in flight to cover the latency.
-      constexpr int U = 8;
-      for (int i0 = tid; i0 < h.m; i0 += U * kCtaThreads) {
-        uint32_t o[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = i0 + u * kCtaThreads;
-          o[u] = i < h.m ? (uint32_t)gperm[i] : 0u;
-        }
-        T vx[U], vy[U], vb[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          pmax = max(pmax, o[u]);
-          const uint32_t oc = min(o[u], (uint32_t)(h.m - 1));
-          vx[u] = gax[oc];
-          vy[u] = gay[oc];
-          vb[u] = gb[oc];
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = i0 + u * kCtaThreads;
-          if (i < h.m) {
-            sbits = max(sbits, float_bits(fabs(vx[u]) + fabs(vy[u])));
-            pax[4 + i] = vx[u];
-            pay[4 + i] = vy[u];
-            pb[4 + i] = vb[u];
+  const int64_t G = gridDim.x;
+  auto lp_of = [&](int64_t t) -> int64_t { return t < n_list ? (list ? (int64_t)list[t] : t) : -1; };
+  // considered position k: box constants for k < 4, else staged element perm[k-4]
+  auto pos = [&](int k, T M, T& x, T& y, T& bb) {
+    const bool box = k < 4;
+    const uint32_t o = rperm[box ? 0 : k - 4];
+    x = box ? (k == 0 ? T(1) : (k == 1 ? T(-1) : T(0))) : rax[o];
+    y = box ? (k == 2 ? T(1) : (k == 3 ? T(-1) : T(0))) : ray[o];
+    bb = box ? M : rb[o];
+  };
+  // warp 0's pipeline registers: the next LP's header words and ticket
+  uint32_t hwN = 0, ticket = 0;
+  int64_t lpN = -1;
+  uint64_t policy = 0;
+  if (wid == 0) {
+    policy = policy_evict_first();
+    lpN = lp_of(blockIdx.x);
+    hwN = load_header_word<T>(p, lpN, lane);
+    ticket = atomic_add_if(p.counter, lane == 0);
+    if (lane == 0) mbar_init(&sh.bar, 1);
+  }
+  uint32_t phase = 0;
+  int step = 0;  // test steps so far (selects the ballot buffer)
+  while (true) {
+    // ---- warp 0: stage the LP (header loaded an LP ago) -------------------
+    if (wid == 0) {
+      bool fits;
+      const Header<T> hn = unpack_header_cap<T>(hwN, lpN, cap, fits);
+      if (lane == 0) {
+        sh.hdr = hn;
+        if (hn.lp >= 0) {
+          const uint32_t bt = fits ? round16((uint32_t)hn.m * sizeof(T)) : 0u;
+          const uint32_t bp = fits ? round16((uint32_t)hn.m * sizeof(P)) : 0u;
+          mbar_arrive_expect_tx(&sh.bar, 3 * bt + bp);
+          if (bt) {
+            bulk_g2s(rax, static_cast<const T*>(p.ax) + hn.off, bt, &sh.bar, policy);
+            bulk_g2s(ray, static_cast<const T*>(p.ay) + hn.off, bt, &sh.bar, policy);
+            bulk_g2s(rb, static_cast<const T*>(p.b) + hn.off, bt, &sh.bar, policy);
+            bulk_g2s(rperm, static_cast<const P*>(p.perm) + hn.off, bp, &sh.bar, policy);
           }
         }
       }
-    } else if (h.ok) {
-      for (int i = tid; i < h.m; i += kCtaThreads) pmax = max(pmax, (uint32_t)gperm[i]);
+      lpN = lp_of((int64_t)__shfl_sync(kFull, ticket, 0) + G);
+      hwN = load_header_word<T>(p, lpN, lane);
+      ticket = atomic_add_if(p.counter, lane == 0);
     }
-    // block reductions of pmax / sbits (as 32-bit words: max of the high
-    // word then of the low word is the max of the bits for both types)
+    __syncthreads();  // header visible (and the previous LP's reads are done)
+    const Header<T> h = sh.hdr;
+    if (h.lp < 0) break;
+    const int mpos = h.m + 4;
+    const bool fits = h.ok && h.m <= cap;
+    mbar_wait(&sh.bar, phase);
+    phase ^= 1u;
+    // ---- validate the permutation, bound |a| (original order, contiguous) -
+    uint32_t pmax = 0;
+    decltype(float_bits(T(0))) sbits = float_bits(T(1));  // the box's |a|
+    if (fits) {
+      for (int i = tid; i < h.m; i += THREADS) {
+        pmax = max(pmax, (uint32_t)rperm[i]);
+        sbits = max(sbits, float_bits(fabs(rax[i]) + fabs(ray[i])));
+      }
+    } else if (h.ok) {
+      const P* gperm = static_cast<const P*>(p.perm) + h.off;
+      for (int i = tid; i < h.m; i += THREADS) pmax = max(pmax, (uint32_t)gperm[i]);
+    }
     pmax = __reduce_max_sync(kFull, pmax);
     const auto sb_w = reduce_max_bits(sbits);
     if (lane == 0) {
@@ -1206,14 +1314,17 @@ __global__ void __launch_bounds__(kCtaThreads) k_solve_cta(const KParams p, int3
       sh.redk[wid][2] = (uint32_t)(unsigned long long)sb_w;
     }
     __syncthreads();
-    uint32_t pm_all = 0;
-    decltype(float_bits(T(0))) sb_all = 0;
-    for (int w = 0; w < kCtaWarps; ++w) {
-      pm_all = max(pm_all, sh.redk[w][0]);
-      decltype(float_bits(T(0))) v;
-      if constexpr (sizeof(T) == 8) v = ((unsigned long long)sh.redk[w][1] << 32) | sh.redk[w][2];
-      else v = sh.redk[w][2];
-      sb_all = max(sb_all, v);
+    uint32_t pm_all;
+    decltype(float_bits(T(0))) sb_all;
+    {
+      pm_all = __reduce_max_sync(kFull, lane < W ? sh.redk[lane][0] : 0u);
+      if constexpr (sizeof(T) == 8) {
+        const unsigned long long v =
+            lane < W ? (((unsigned long long)sh.redk[lane][1] << 32) | sh.redk[lane][2]) : 0ull;
+        sb_all = reduce_max_bits(v);
+      } else {
+        sb_all = __reduce_max_sync(kFull, lane < W ? sh.redk[lane][2] : 0u);
+      }
     }
     const bool bad = !h.ok || (h.m > 0 && pm_all >= (uint32_t)h.m);
     const T m_all = float_from_bits<T>(sb_all);
@@ -1224,47 +1335,59 @@ __global__ void __launch_bounds__(kCtaThreads) k_solve_cta(const KParams p, int3
     S.st = bad ? 255 : 0;
     const T cthr = eps_par * sqrt(h.cx * h.cx + h.cy * h.cy);
     bool need_exact = !bad && wild;
-    // ---- sweep -------------------------------------------------------------
+    // ---- sweep (serial.hpp:168-186) ----------------------------------------
     int start = 4;  // first position to test
     bool running = !bad && !wild;
     while (running) {
       int pi = -1;
-      for (int base = start & ~(kCtaThreads - 1); base < mpos; base += kCtaThreads) {
+      for (int base = start & ~(THREADS - 1); base < mpos; base += THREADS) {
         const int P_ = base + tid;
-        const bool v = P_ >= start && P_ < mpos &&
-                       !satisfied(pax[P_], pay[P_], pb[P_], S.px, S.py, eps_feas);
-        const uint32_t bm = __ballot_sync(kFull, v);
-        __syncthreads();  // previous step's readers of sh.bal are done
-        if (lane == 0) sh.bal[wid] = bm;
-        __syncthreads();
-        for (int w = 0; w < kCtaWarps; ++w) {
-          const uint32_t b = sh.bal[w];
-          if (b) {
-            pi = base + 32 * w + __ffs(b) - 1;
-            break;
-          }
+        bool v = false;
+        if (P_ >= start && P_ < mpos) {
+          T x, y, bb;
+          pos(P_, h.M, x, y, bb);
+          v = !satisfied(x, y, bb, S.px, S.py, eps_feas);
         }
-        if (pi >= 0) break;
+        const uint32_t bm = __ballot_sync(kFull, v);
+        uint32_t* bal = sh.bal[step & 1];
+        ++step;
+        if (lane == 0) bal[wid] = bm;
+        __syncthreads();
+        const uint32_t wb = lane < W ? bal[lane] : 0u;
+        const uint32_t nz = __ballot_sync(kFull, wb != 0u);
+        if (nz) {
+          const int w = __ffs(nz) - 1;
+          pi = base + 32 * w + __ffs(__shfl_sync(kFull, wb, w)) - 1;
+          break;
+        }
       }
       if (pi < 0) break;
       // ---- event at position pi ------------------------------------------
       S.viol += 1;
       S.wu += (uint32_t)pi;
-      const Line<T> l = boundary_of(pax[pi], pay[pi], pb[pi]);
+      T hx, hy, hb;
+      pos(pi, h.M, hx, hy, hb);
+      const Line<T> l = boundary_of(hx, hy, hb);
       Acc<T> acc;
       acc.uL = -T(INFINITY);
       acc.uR = T(INFINITY);
       acc.oL = acc.oR = acc.par = kNone;
       bool rare = false;
-      for (int k = tid; k < pi; k += kCtaThreads)
-        wu_fold(pax[k], pay[k], pb[k], l, lpbnd, (uint32_t)k, true, acc, rare);
-      bool rare_cta = __syncthreads_or(rare);
-      if (rare_cta) {  // exact reference classify for every unit (rare)
+#pragma unroll 2
+      for (int k = tid; k < pi; k += THREADS) {
+        T x, y, bb;
+        pos(k, h.M, x, y, bb);
+        wu_fold(x, y, bb, l, lpbnd, (uint32_t)k, true, acc, rare);
+      }
+      if (__syncthreads_or(rare)) {  // exact reference classify for every unit (rare)
         acc.uL = -T(INFINITY);
         acc.uR = T(INFINITY);
         acc.oL = acc.oR = acc.par = kNone;
-        for (int k = tid; k < pi; k += kCtaThreads)
-          wu_apply(pax[k], pay[k], pb[k], l, eps_par, eps_feas, eps_hi, (uint32_t)k, acc);
+        for (int k = tid; k < pi; k += THREADS) {
+          T x, y, bb;
+          pos(k, h.M, x, y, bb);
+          wu_apply(x, y, bb, l, eps_par, eps_feas, eps_hi, (uint32_t)k, acc);
+        }
       }
       const Merged<T> mw = merge_lanes(acc, true);
       if (lane == 0) {
@@ -1275,29 +1398,16 @@ __global__ void __launch_bounds__(kCtaThreads) k_solve_cta(const KParams p, int3
         sh.par[wid] = mw.par;
       }
       __syncthreads();
-      // Merge the warps' extremes (value equality ties keep the smaller
-      // position, as the serial fold does).
-      Merged<T> mg;
-      mg.uL = -T(INFINITY);
-      mg.uR = T(INFINITY);
-      mg.oL = mg.oR = mg.par = kNone;
-      for (int w = 0; w < kCtaWarps; ++w) {
-        const T vl = sh.vL[w], vr = sh.vR[w];
-        if (vl > mg.uL) {
-          mg.uL = vl;
-          mg.oL = sh.oL[w];
-        } else if (vl == mg.uL) {
-          mg.oL = min(mg.oL, sh.oL[w]);
-        }
-        if (vr < mg.uR) {
-          mg.uR = vr;
-          mg.oR = sh.oR[w];
-        } else if (vr == mg.uR) {
-          mg.oR = min(mg.oR, sh.oR[w]);
-        }
-        mg.par = min(mg.par, sh.par[w]);
-      }
-      __syncthreads();  // the shared merge slots are reused by the next event
+      // Merge the warps' extremes the same way (value ties keep the smaller
+      // position, as the serial fold does). The slots are rewritten only
+      // after the next test step's barrier.
+      Acc<T> aw;
+      aw.uL = lane < W ? sh.vL[lane] : -T(INFINITY);
+      aw.uR = lane < W ? sh.vR[lane] : T(INFINITY);
+      aw.oL = lane < W ? sh.oL[lane] : kNone;
+      aw.oR = lane < W ? sh.oR[lane] : kNone;
+      aw.par = lane < W ? sh.par[lane] : kNone;
+      const Merged<T> mg = merge_lanes(aw, true);
       if (!resolve_merged(S, mg, l, (uint32_t)pi, h, cthr, eps_feas)) break;
       if (!(fabs(S.px) < T(INFINITY) && fabs(S.py) < T(INFINITY))) {
         need_exact = true;
@@ -1313,9 +1423,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_solve_cta(const KParams p, int3
       if (st == 0 && (S.pos0 < 4 || S.pos1 < 4)) st = 2;
       write_result<T, P>(p, h, st, S.px, S.py, S.pos0, S.pos1, S.viol, S.wu);
     }
-    __syncthreads();
-    j = sh.lp_next;
-    __syncthreads();
+    fence_proxy_async_smem();  // this LP's reads before the next LP's TMA
   }
   if (tid == 0) {
     __threadfence();
@@ -1326,6 +1434,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_solve_cta(const KParams p, int3
     }
   }
 }
+
 
 // Large LPs (m above the register classes) and any other LP: one warp per
 // LP straight from global memory (solve_exact_global), claimed dynamically.
@@ -1390,20 +1499,28 @@ __device__ __forceinline__ int size_class(int32_t m, const int32_t* slots, int n
   return nreg;
 }
 
-constexpr int kMaxBins = 64;
+constexpr int kMaxBins = 128;
 
 struct BinSpec {
   int32_t slots[8];
   int32_t nreg;
   int32_t lane_bins;  // > 0: class 0 is split into one bin per m in [0, lane_bins)
+  int32_t cta_bins;   // > 1: the large class is split by m, largest first
+  int32_t cta_lo, cta_width;
 };
 
-// Bin of an LP: class 0 -> bin m (lane kernel) or 0; class c -> c + lane_bins - 1.
+// Bin of an LP. Bins in list order: class 0 (one bin per m when the lane
+// kernel runs it, ascending), classes 1..nreg-1 (one bin each), the large
+// class (cta_bins bins of cta_width sizes, DEScending m: longest LPs first).
 __device__ __forceinline__ int bin_of(int32_t m, const BinSpec& spec) {
   const int c = size_class(m, spec.slots, spec.nreg);
-  if (spec.lane_bins == 0) return c;
-  if (c == 0) return min(max(m, 0), spec.lane_bins - 1);
-  return c + spec.lane_bins - 1;
+  const int b0 = spec.lane_bins ? spec.lane_bins : 1;
+  if (c == 0) return spec.lane_bins ? min(max(m, 0), spec.lane_bins - 1) : 0;
+  if (c < spec.nreg) return b0 + c - 1;
+  const int base = b0 + spec.nreg - 1;
+  if (spec.cta_bins <= 1) return base;
+  const int q = min((max(m, spec.cta_lo) - spec.cta_lo) / spec.cta_width, spec.cta_bins - 1);
+  return base + spec.cta_bins - 1 - q;
 }
 
 __global__ void k_bin_count(int64_t n, const int32_t* m, BinSpec spec, int32_t* counts) {
