@@ -114,6 +114,12 @@ struct WarpLayout {
                              : (blocks_for(kWarps) < LP2D_MIN_BLOCKS ? blocks_for(kWarps)
                                                                      : LP2D_MIN_BLOCKS);
   static constexpr uint32_t kSmem = kWarps * kBuf + kWarps * 8;
+  // Register chunks below this index are never past the end of an LP of this
+  // size class (m + 4 > 32 * previous class's chunks), so their test needs
+  // no bound check.
+  static constexpr int kAlwaysValid =
+      NT > 0 ? NS
+             : (NS == 2 ? 1 : NS == 3 ? 2 : NS == 5 ? 3 : NS == 9 ? 5 : NS == 17 ? 9 : 0);
 };
 
 // Per-LP header held by lane 0 between claim and solve.
@@ -502,7 +508,8 @@ __device__ __noinline__ void solve_exact_global(const KParams& p, const Header<T
 #define LP2D_TEST_CASE(K)                                                   \
   case K:                                                                   \
     if constexpr (K < NS) {                                                 \
-      if (32 * K >= mpos) break;                                            \
+      if constexpr (K >= L::kAlwaysValid)                                   \
+        if (32 * K >= mpos) break;                                          \
       const bool v = !satisfied(rax[K], ray[K], rb[K], px, py, eps_feas);   \
       uint32_t vm = __ballot_sync(kFull, v) & startmask;                    \
       startmask = kFull;                                                    \
@@ -974,7 +981,7 @@ __device__ __forceinline__ Line<T> shfl_line(const Line<T>& l, int src) {
 
 template <typename T, typename P, int MAXM>
 __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const KParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   using LT = LaneTile<T, MAXM>;
   constexpr int ST = LT::kStride;
   const int lane = threadIdx.x & 31, wic = threadIdx.x >> 5;
