@@ -138,6 +138,25 @@ int lp2dgpu_shuffle_device(int64_t n, const int32_t* m, const int64_t* offset,
                            const uint64_t* seeds, void* perm, int32_t perm_bits,
                            int32_t device, void* stream);
 
+/* ---- contention microbenchmark -------------------
+ * Segmented extremes: out_min[g] / out_max[g] = min / max of the g-th
+ * consecutive group of `contention` values of in[0..n) — replaces
+ * lp2d::segmented_extremes (reduction.hpp:46-129) with the GPU update
+ * disciplines of the paper's Fig. atomicComp. Every strategy returns the
+ * same values (min/max are exact); NaNs are ignored like std::fmin/fmax.
+ * Device pointers, enqueued on `stream`. Errors as reduction.hpp:52-64
+ * (contention < 1, n not a multiple of contention: LP2D_ERR_ARG). */
+enum {
+  LP2D_REDUCE_SHARED_ATOMIC = 0, /* shared-memory atomics (serialized update) */
+  LP2D_REDUCE_TREE = 1,          /* halving-stride tree in shared memory      */
+  LP2D_REDUCE_PRIVATE_MERGE = 2, /* private partials, merged per warp         */
+  LP2D_REDUCE_GLOBAL_ATOMIC = 3, /* global-memory atomics                     */
+  LP2D_REDUCE_CUB = 4,           /* cub::DeviceSegmentedReduce (library)      */
+};
+int lp2dgpu_segmented_extremes(const double* in, int64_t n, int64_t contention,
+                               int32_t strategy, double* out_min, double* out_max,
+                               int32_t device, void* stream);
+
 /* Number of visible CUDA devices (0 when none). */
 int lp2dgpu_device_count(void);
 

@@ -48,6 +48,12 @@ int lp2dgen_fill(int64_t n, int64_t first, uint64_t seed, const int32_t* m,
                  double bscale, double* ax, double* ay, double* b,
                  uint32_t* perm, double* c, double* bound_m, int threads);
 
+/* n draws of xoshiro256pp(derive_seed(seed, stream)).in_range(lo, hi)
+ * (rng.hpp:42) — the contention benchmark's inputs with stream 0xC0
+ * (bench.hpp:256-257). */
+void lp2dgen_uniform(uint64_t seed, uint64_t stream, double lo, double hi, int64_t n,
+                     double* out);
+
 /* Heavy-tailed sizes: m_j = clamp(floor(xmin /
  * u^(1/alpha)), xmin, xmax) with u = xoshiro256pp(derive_seed(seed, 0xB0))
  * .unit() drawn in sequence, until sum(m) >= target or n_max reached.

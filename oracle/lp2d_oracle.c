@@ -342,3 +342,77 @@ int lp2d_oracle_bruteforce(const double* cax, const double* cay,
   out->value = bv;
   return 0;
 }
+
+/* ---- reduction.hpp:46-129 segmented_extremes --------------------------------
+ * Each consecutive group of `contention` values reduced to min and max under
+ * the reference's three update disciplines (0 serialized, 1 tree, 2 private
+ * partials then merge). fmin/fmax as std::fmin/std::fmax. Returns -1 on the
+ * reference's invalid_argument cases. */
+int lp2d_oracle_segmented_extremes(const double* in, int64_t n, int64_t contention,
+                                   int strategy, double* out_min, double* out_max) {
+  if (contention <= 0 || n % contention != 0) return -1;
+  const int64_t groups = n / contention;
+  const int64_t c = contention;
+  double* mn = NULL;
+  double* mx = NULL;
+  if (strategy == 1 || strategy == 2) {
+    mn = (double*)malloc(sizeof(double) * (size_t)(c > 32 ? c : 32));
+    mx = (double*)malloc(sizeof(double) * (size_t)(c > 32 ? c : 32));
+  }
+  for (int64_t g = 0; g < groups; ++g) {
+    const double* v = in + g * c;
+    if (strategy == 0) { /* serialized shared update, reduction.hpp:66-78 */
+      double a = v[0], b = v[0];
+      for (int64_t i = 1; i < c; ++i) {
+        a = fmin(a, v[i]);
+        b = fmax(b, v[i]);
+      }
+      out_min[g] = a;
+      out_max[g] = b;
+    } else if (strategy == 1) { /* halving tree, reduction.hpp:80-97 */
+      for (int64_t i = 0; i < c; ++i) mn[i] = mx[i] = v[i];
+      int64_t s = 1;
+      while (s < c) s <<= 1;
+      for (s >>= 1; s >= 1; s >>= 1) {
+        for (int64_t i = 0; i < s; ++i)
+          if (i + s < c) {
+            mn[i] = fmin(mn[i], mn[i + s]);
+            mx[i] = fmax(mx[i], mx[i + s]);
+          }
+        if (s == 1) break;
+      }
+      out_min[g] = mn[0];
+      out_max[g] = mx[0];
+    } else { /* private partials then merge, reduction.hpp:99-125 */
+      const int64_t lanes = c < 32 ? c : 32;
+      for (int64_t l = 0; l < lanes; ++l) {
+        double a = v[l], b = v[l];
+        for (int64_t i = l + lanes; i < c; i += lanes) {
+          a = fmin(a, v[i]);
+          b = fmax(b, v[i]);
+        }
+        mn[l] = a;
+        mx[l] = b;
+      }
+      double a = mn[0], b = mx[0];
+      for (int64_t l = 1; l < lanes; ++l) {
+        a = fmin(a, mn[l]);
+        b = fmax(b, mx[l]);
+      }
+      out_min[g] = a;
+      out_max[g] = b;
+    }
+  }
+  free(mn);
+  free(mx);
+  return 0;
+}
+
+/* bench.hpp:256-257: the contention benchmark's inputs,
+ * xoshiro256pp(derive_seed(seed, stream)).in_range(lo, hi) drawn n times. */
+void lp2d_oracle_uniform(uint64_t seed, uint64_t stream, double lo, double hi, int64_t n,
+                         double* out) {
+  xoshiro r;
+  xo_seed(&r, lp2d_oracle_derive_seed(seed, stream));
+  for (int64_t i = 0; i < n; ++i) out[i] = xo_in_range(&r, lo, hi);
+}

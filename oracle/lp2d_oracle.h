@@ -81,6 +81,14 @@ int lp2d_oracle_bruteforce(const double* ax, const double* ay, const double* b,
                            double eps_par, double eps_feas,
                            lp2d_oracle_result* out);
 
+/* reduction.hpp:46-129 segmented_extremes (strategy 0 serialized, 1 tree,
+ * 2 private-then-merge); -1 on the reference's invalid_argument cases. */
+int lp2d_oracle_segmented_extremes(const double* in, int64_t n, int64_t contention,
+                                   int strategy, double* out_min, double* out_max);
+/* bench.hpp:256-257 inputs: xoshiro256pp(derive_seed(seed, stream)).in_range */
+void lp2d_oracle_uniform(uint64_t seed, uint64_t stream, double lo, double hi, int64_t n,
+                         double* out);
+
 #ifdef __cplusplus
 }
 #endif

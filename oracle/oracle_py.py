@@ -77,6 +77,10 @@ def oracle_lib():
             fn = getattr(lib, "lp2d_oracle_solve_batch_" + suf)
             fn.argtypes = [C.c_int64] + [C.c_void_p] * 8 + [C.c_double, C.c_double, C.c_int, C.c_void_p]
         lib.lp2d_oracle_bruteforce.argtypes = [C.c_void_p] * 3 + [C.c_int64] + [C.c_double] * 5 + [C.c_void_p]
+        lib.lp2d_oracle_segmented_extremes.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                                                       C.c_void_p, C.c_void_p]
+        lib.lp2d_oracle_uniform.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_int64,
+                                            C.c_void_p]
         _oracle = lib
     return _oracle
 
@@ -109,6 +113,10 @@ def ref_lib():
         lib.ref_batch_solve_serial_threads.argtypes = [C.c_void_p, C.c_uint, C.c_double, C.c_double] + [C.c_void_p] * 4
         lib.ref_verify.restype = C.c_int64
         lib.ref_verify.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_int64]
+        lib.ref_segmented_extremes.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]
+        lib.ref_uniform.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_int64, C.c_void_p]
+        lib.ref_contention_ns.restype = C.c_int64
+        lib.ref_contention_ns.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_uint64, C.c_int64]
         _ref = lib
     return _ref
 
@@ -162,4 +170,25 @@ def bruteforce(ax, ay, b, c, M, eps_par=1e-12, eps_feas=1e-9):
                                             eps_par, eps_feas, C.byref(out))
     if rc:
         raise ValueError("bruteforce: instance larger than the oracle cap")
+    return out
+
+
+# ---- contention microbenchmark (reduction.hpp, bench.hpp:244-274) ----------
+
+def segmented_extremes(values, contention, strategy, ref=False):
+    """(mins, maxs) of consecutive groups; strategy 0 serialized, 1 tree,
+    2 private-then-merge. ref=True runs the compiled reference."""
+    v = np.ascontiguousarray(values, np.float64)
+    g = len(v) // contention if contention > 0 else 0
+    mn = np.zeros(max(g, 1)); mx = np.zeros(max(g, 1))
+    fn = ref_lib().ref_segmented_extremes if ref else oracle_lib().lp2d_oracle_segmented_extremes
+    if fn(_p(v), len(v), contention, strategy, _p(mn), _p(mx)):
+        raise ValueError("segmented_extremes: bad shape")
+    return mn[:g], mx[:g]
+
+
+def uniform(seed, stream, lo, hi, n, ref=False):
+    out = np.zeros(n)
+    fn = ref_lib().ref_uniform if ref else oracle_lib().lp2d_oracle_uniform
+    fn(seed & (2**64 - 1), stream & (2**64 - 1), lo, hi, n, _p(out))
     return out

@@ -9,10 +9,13 @@
 // Packed layout (same as the product C-ABI): LP j owns elements
 // [offset[j], offset[j] + m[j]) of ax/ay/b/perm (perm widened to u32).
 
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <span>
+#include <stdexcept>
 #include <vector>
 
 #include "lp2d/bench.hpp"
@@ -252,6 +255,43 @@ int64_t ref_verify(int64_t count, int64_t max_size, uint64_t seed,
   const auto rep = lp2d::bench::verify(static_cast<std::size_t>(count),
                                        static_cast<std::size_t>(max_size), opts);
   return static_cast<int64_t>(rep.disagreements);
+}
+
+// reduction.hpp:46 segmented_extremes; -1 when it throws invalid_argument.
+int ref_segmented_extremes(const double* in, int64_t n, int64_t contention, int strategy,
+                           double* out_min, double* out_max) {
+  const std::size_t groups = contention > 0 ? static_cast<std::size_t>(n / contention) : 0;
+  try {
+    lp2d::segmented_extremes(std::span<const double>(in, static_cast<std::size_t>(n)),
+                             static_cast<std::size_t>(contention),
+                             static_cast<lp2d::reduce_strategy>(strategy),
+                             std::span<double>(out_min, groups), std::span<double>(out_max, groups));
+  } catch (const std::invalid_argument&) {
+    return -1;
+  }
+  return 0;
+}
+
+// bench.hpp:256-257 contention inputs.
+void ref_uniform(uint64_t seed, uint64_t stream, double lo, double hi, int64_t n, double* out) {
+  lp2d::xoshiro256pp rng(lp2d::derive_seed(seed, stream));
+  for (int64_t i = 0; i < n; ++i) out[i] = rng.in_range(lo, hi);
+}
+
+// bench::contention_bench: the reference's own CPU timing of one strategy at
+// one contention level (ns per pass, median of reps).
+int64_t ref_contention_ns(int strategy, int64_t contention, int64_t reps, uint64_t seed,
+                          int64_t values) {
+  const lp2d::reduce_strategy s = static_cast<lp2d::reduce_strategy>(strategy);
+  const std::size_t c = static_cast<std::size_t>(contention);
+  const auto recs = lp2d::bench::contention_bench(std::span<const lp2d::reduce_strategy>(&s, 1),
+                                                  std::span<const std::size_t>(&c, 1),
+                                                  static_cast<std::size_t>(reps), seed,
+                                                  static_cast<std::size_t>(values));
+  std::vector<int64_t> t;
+  for (const auto& r : recs) t.push_back(r.wall_time_ns);
+  std::sort(t.begin(), t.end());
+  return t.empty() ? 0 : t[t.size() / 2];
 }
 
 }  // extern "C"

@@ -32,6 +32,8 @@ MEM_HOST, MEM_DEVICE = 0, 1
 SCHED_NAIVE, SCHED_BALANCED = 0, 1
 
 GEN_FEASIBLE, GEN_INFEASIBLE, GEN_UNBOUNDED = 0, 1, 3
+(REDUCE_SHARED_ATOMIC, REDUCE_TREE, REDUCE_PRIVATE_MERGE, REDUCE_GLOBAL_ATOMIC,
+ REDUCE_CUB) = range(5)
 
 
 class BatchSoA(C.Structure):
@@ -86,6 +88,7 @@ EXPORTS = (
     "lp2dgpu_shuffle_device",
     "lp2dgpu_device_count",
     "lp2dgpu_kernel_launches",
+    "lp2dgpu_segmented_extremes",
     "lp2dgpu_last_error",
     "lp2dgpu_version",
     "lp2dgen_derive_seed",
@@ -93,6 +96,7 @@ EXPORTS = (
     "lp2dgen_gen",
     "lp2dgen_fill",
     "lp2dgen_pareto_sizes",
+    "lp2dgen_uniform",
 )
 
 _lib = None
@@ -130,8 +134,13 @@ def lib():
     L.lp2dgpu_shuffle_device.restype = C.c_int
     L.lp2dgpu_device_count.restype = C.c_int
     L.lp2dgpu_kernel_launches.restype = C.c_uint64
+    L.lp2dgpu_segmented_extremes.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int32,
+                                             C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+    L.lp2dgpu_segmented_extremes.restype = C.c_int
     L.lp2dgpu_last_error.restype = C.c_char_p
     L.lp2dgpu_version.restype = C.c_char_p
+    L.lp2dgen_uniform.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_int64,
+                                  C.c_void_p]
     L.lp2dgen_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
     L.lp2dgen_derive_seed.restype = C.c_uint64
     L.lp2dgen_shuffle.argtypes = [C.c_int64, C.c_uint64, C.c_void_p]

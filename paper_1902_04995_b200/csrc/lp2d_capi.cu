@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -17,6 +18,7 @@
 
 #include "../../include/lp2d_b200.h"
 #include "lp2d_kernels.cuh"
+#include "lp2d_reduce.cuh"
 
 using namespace lp2d_b200;
 
@@ -639,6 +641,91 @@ int lp2dgpu_shuffle_device(int64_t n, const int32_t* m, const int64_t* offset,
   else
     return fail(LP2D_ERR_ARG, "perm_bits must be 16 or 32");
   note_launch();
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int lp2dgpu_segmented_extremes(const double* in, int64_t n, int64_t contention, int32_t strategy,
+                               double* out_min, double* out_max, int32_t device, void* stream) {
+  // reduction.hpp:52-64 validation, as codes
+  if (contention <= 0) return fail(LP2D_ERR_ARG, "segmented_extremes: contention must be >= 1");
+  if (n < 0 || n % contention != 0)
+    return fail(LP2D_ERR_ARG, "segmented_extremes: input size must be a multiple of contention");
+  if (strategy < LP2D_REDUCE_SHARED_ATOMIC || strategy > LP2D_REDUCE_CUB)
+    return fail(LP2D_ERR_ARG, "segmented_extremes: unknown strategy");
+  const int64_t groups = n / contention;
+  if (groups == 0) return 0;
+  if (!in || !out_min || !out_max) return fail(LP2D_ERR_ARG, "null argument");
+  DeviceGuard guard;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(LP2D_ERR_CUDA, "no CUDA device visible (the solver has no CPU fallback)");
+  if (device < 0 || device >= ndev) return fail(LP2D_ERR_ARG, "bad device");
+  CUDA_TRY(cudaSetDevice(device));
+  if (int rc = ensure_device(device)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t c = contention;
+  const int64_t cap = (int64_t)g_dev[device].sm_count * 4;
+  switch (strategy) {
+    case LP2D_REDUCE_SHARED_ATOMIC: {
+      const int64_t G = groups_per_block(c);
+      const int grid = (int)std::min<int64_t>((groups + G - 1) / G, cap);
+      k_ext_shared_atomic<<<grid, kReduceThreads, 0, s>>>(in, groups, c, out_min, out_max);
+      note_launch();
+      break;
+    }
+    case LP2D_REDUCE_TREE: {
+      const int64_t G = groups_per_block(c);
+      const int grid = (int)std::min<int64_t>((groups + G - 1) / G, cap);
+      k_ext_tree<<<grid, kReduceThreads, 0, s>>>(in, groups, c, out_min, out_max);
+      note_launch();
+      break;
+    }
+    case LP2D_REDUCE_PRIVATE_MERGE: {
+      const int64_t lanes = std::min<int64_t>(c, 32);
+      if (32 % lanes == 0) {
+        const int grid = (int)std::min<int64_t>((groups * lanes + kReduceThreads - 1) / kReduceThreads, cap);
+        k_ext_private_shfl<<<grid, kReduceThreads, 0, s>>>(in, groups, c, out_min, out_max);
+      } else {
+        const int64_t per = kReduceThreads / lanes;
+        const int grid = (int)std::min<int64_t>((groups + per - 1) / per, cap);
+        k_ext_private<<<grid, kReduceThreads, 0, s>>>(in, groups, c, out_min, out_max);
+      }
+      note_launch();
+      break;
+    }
+    case LP2D_REDUCE_GLOBAL_ATOMIC: {
+      const int gg = (int)std::min<int64_t>((groups + 255) / 256, cap);
+      const int gn = (int)std::min<int64_t>((n + 255) / 256, cap * 2);
+      k_ext_global_init<<<gg, 256, 0, s>>>(groups, out_min, out_max);
+      k_ext_global_atomic<<<gn, 256, 0, s>>>(in, n, c, out_min, out_max);
+      k_ext_global_fini<<<gg, 256, 0, s>>>(groups, out_min, out_max);
+      note_launch();
+      note_launch();
+      note_launch();
+      break;
+    }
+    case LP2D_REDUCE_CUB: {
+      cub::CountingInputIterator<int64_t> count(0);
+      cub::TransformInputIterator<int64_t, GroupOffset, cub::CountingInputIterator<int64_t>> begin(
+          count, GroupOffset{c});
+      const double qnan = std::numeric_limits<double>::quiet_NaN();  // fmin/fmax identity
+      size_t b1 = 0, b2 = 0;
+      CUDA_TRY(cub::DeviceSegmentedReduce::Reduce(nullptr, b1, in, out_min, groups, begin, begin + 1,
+                                                  NanMinOp{}, qnan, s));
+      CUDA_TRY(cub::DeviceSegmentedReduce::Reduce(nullptr, b2, in, out_max, groups, begin, begin + 1,
+                                                  NanMaxOp{}, qnan, s));
+      void* tmp = nullptr;
+      const size_t tb = std::max<size_t>(std::max(b1, b2), 16);
+      CUDA_TRY(cudaMallocFromPoolAsync(&tmp, tb, g_dev[device].pool, s));
+      CUDA_TRY(cub::DeviceSegmentedReduce::Reduce(tmp, b1, in, out_min, groups, begin, begin + 1,
+                                                  NanMinOp{}, qnan, s));
+      CUDA_TRY(cub::DeviceSegmentedReduce::Reduce(tmp, b2, in, out_max, groups, begin, begin + 1,
+                                                  NanMaxOp{}, qnan, s));
+      CUDA_TRY(cudaFreeAsync(tmp, s));
+      break;
+    }
+  }
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -170,6 +170,12 @@ int lp2dgen_fill(int64_t n, int64_t first, uint64_t seed, const int32_t* m,
   return 0;
 }
 
+void lp2dgen_uniform(uint64_t seed, uint64_t stream, double lo, double hi, int64_t n,
+                     double* out) {
+  Rng r(lp2dgen_derive_seed(seed, stream));
+  for (int64_t i = 0; i < n; ++i) out[i] = r.in_range(lo, hi);
+}
+
 int64_t lp2dgen_pareto_sizes(uint64_t seed, double xmin, double alpha, int32_t xmax,
                              int64_t target_total, int64_t n_max, int32_t* m) {
   Rng r(lp2dgen_derive_seed(seed, 0xB0));

@@ -14,6 +14,11 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
 
 
+requires_ref = pytest.mark.skipif(
+    not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "liblp2d_ref.so")),
+    reason="oracle/_ref (the compiled reference) not built")
+
+
 def cuda_available():
     try:
         import torch
