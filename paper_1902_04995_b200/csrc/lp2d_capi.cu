@@ -107,11 +107,11 @@ uint32_t* take_counter(int dev) {
 }
 
 // Register slot classes: NS slots hold m + 4 positions (box included).
-constexpr int kSlotClasses[] = {1, 2, 3, 5, 9, 17, 33};
+constexpr int kSlotClasses[] = {1, 2, 4, 6, 10, 18, 33};
 
 template <typename T>
 constexpr int max_nslot() {
-  return sizeof(T) == 4 ? 33 : 17;  // fp64 keeps m <= 540 in registers
+  return sizeof(T) == 4 ? 33 : 18;  // fp64 keeps m <= 572 in registers
 }
 
 // Eps_par rounded up by 2^-10 (relative), in T: the parallel-filter factor.
@@ -264,12 +264,12 @@ int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t ma
       if (tiny_uses_lanes()) return launch_lane_kernel<T, P>(kp, dev, s);
       return launch_warp_kernel<T, P, 1>(kp, dev, s);
     case 2: return launch_warp_kernel<T, P, 2>(kp, dev, s);
-    case 3: return launch_warp_kernel<T, P, 3>(kp, dev, s);
-    case 5: return launch_warp_kernel<T, P, 5>(kp, dev, s);
-    case 9: return launch_warp_kernel<T, P, 9>(kp, dev, s);
-    case 17: return launch_warp_kernel<T, P, 17>(kp, dev, s);
-    case 33:  // 17 register chunks + 16 shared-memory tail chunks
-      if constexpr (max_nslot<T>() >= 33) return launch_warp_kernel<T, P, 17, 16>(kp, dev, s);
+    case 4: return launch_warp_kernel<T, P, 4>(kp, dev, s);
+    case 6: return launch_warp_kernel<T, P, 6>(kp, dev, s);
+    case 10: return launch_warp_kernel<T, P, 10>(kp, dev, s);
+    case 18: return launch_warp_kernel<T, P, 18>(kp, dev, s);
+    case 33:  // 16 register chunks + 17 shared-memory tail chunks
+      if constexpr (max_nslot<T>() >= 33) return launch_warp_kernel<T, P, 16, 17>(kp, dev, s);
       break;
   }
   return fail(LP2D_ERR_UNSUPPORTED, "size class not built");
@@ -411,6 +411,9 @@ KParams make_params(const lp2d_opts* o) {
   kp.eps_par_f = (float)kp.eps_par;
   kp.eps_feas_f = (float)kp.eps_feas;
   kp.eps_hi_f = (float)kp.eps_hi;
+  kp.pk.nz = 0x8000000080000000ull;    // (-0.f, -0.f)
+  kp.pk.one = 0x3f8000003f800000ull;   // (1.f, 1.f)
+  kp.pk.zero = 0;                      // (+0.f, +0.f)
   return kp;
 }
 

@@ -25,6 +25,7 @@
 #include <type_traits>
 
 #include "lp2d_device.cuh"
+#include "lp2d_pair.cuh"
 
 namespace lp2d_b200 {
 
@@ -62,6 +63,7 @@ struct KParams {
   double eps_par, eps_feas, eps_hi;   // tolerance rounded to the scalar type
   float eps_par_f, eps_feas_f, eps_hi_f;  // (float copies: constant-bank operands)
   int32_t total_warps;
+  PairConsts pk;  // packed-fp32 constants (lp2d_pair.cuh)
 };
 
 template <typename T>
@@ -119,7 +121,7 @@ struct WarpLayout {
   // no bound check.
   static constexpr int kAlwaysValid =
       NT > 0 ? NS
-             : (NS == 2 ? 1 : NS == 3 ? 2 : NS == 5 ? 3 : NS == 9 ? 5 : NS == 17 ? 9 : 0);
+             : (NS == 2 ? 1 : NS == 4 ? 2 : NS == 6 ? 4 : NS == 10 ? 6 : NS == 18 ? 10 : 0);
 };
 
 // Per-LP header held by lane 0 between claim and solve.
@@ -501,348 +503,7 @@ __device__ __noinline__ void solve_exact_global(const KParams& p, const Header<T
   }
 }
 
-// One case of the violation-test dispatch: test slot K (compile-time) against
-// the current optimum; on the first violated lane leave the switch with
-// sfound = K. Entering the switch at `case s` resumes the sweep where the
-// previous event left it (Duff's device), so no code runs for earlier slots.
-#define LP2D_TEST_CASE(K)                                                   \
-  case K:                                                                   \
-    if constexpr (K < NS) {                                                 \
-      if constexpr (K >= L::kAlwaysValid)                                   \
-        if (32 * K >= mpos) break;                                          \
-      const bool v = !satisfied(rax[K], ray[K], rb[K], px, py, eps_feas);   \
-      uint32_t vm = __ballot_sync(kFull, v) & startmask;                    \
-      startmask = kFull;                                                    \
-      hx = opaque_copy(rax[K]);                                             \
-      hy = opaque_copy(ray[K]);                                             \
-      hb = opaque_copy(rb[K]);                                              \
-      if (vm) {                                                             \
-        vfound = vm;                                                        \
-        sfound = K;                                                         \
-        break;                                                              \
-      }                                                                     \
-    }                                                                       \
-    [[fallthrough]];
-
-template <typename T, typename P, int NS, int NT>
-__global__ void __launch_bounds__(WarpLayout<T, P, NS, NT>::kWarps * 32,
-                                  (WarpLayout<T, P, NS, NT>::kMinBlocks))
-    k_solve_warp(const KParams p) {
-  static_assert(NS >= 1 && NS <= 40, "slot count");
-  using L = WarpLayout<T, P, NS, NT>;
-  constexpr int W = L::kWarps;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int lane = threadIdx.x & 31;
-  const int wic = threadIdx.x >> 5;
-  unsigned char* buf = smem + wic * L::kBuf;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + W * L::kBuf) + wic;
-  const T* sax = reinterpret_cast<const T*>(buf);
-  const T* say = reinterpret_cast<const T*>(buf + L::kArr);
-  const T* sb = reinterpret_cast<const T*>(buf + 2 * L::kArr);
-  const P* sperm = reinterpret_cast<const P*>(buf + 3 * L::kArr);
-  // tail chunk c, lane -> the staged constraint behind position 32*(NS+c)+lane
-  auto tail_load = [&](int c, T& x, T& y, T& bb) {
-    const int P_ = 32 * (NS + c) + lane;
-    const uint32_t o = min((uint32_t)sperm[min(P_ - 4, L::kCap - 1)], (uint32_t)(L::kCap - 1));
-    x = sax[o];
-    y = say[o];
-    bb = sb[o];
-  };
-
-  const T eps_par = Eps<T>::par(p);
-  const T eps_feas = Eps<T>::feas(p);
-  const T eps_hi = Eps<T>::hi(p);
-  const uint64_t policy = policy_evict_first();
-
-  if (lane == 0) mbar_init(bar, 1);
-  __syncwarp();
-
-  const int32_t* list;
-  int64_t n_list;
-  resolve_list(p, list, n_list);
-  uint32_t phase = 0;
-  // Software pipeline per warp, one stage per solved LP so no long-latency
-  // result is consumed in the iteration that requested it:
-  //   ticket (atomic, lane 0) -> header fields (lane-distributed loads)
-  //   -> TMA of the segments -> gather + solve.
-  // The first two LPs of a warp are static (warp id, warp id + #warps).
-  const int64_t TW = p.total_warps;
-  const int64_t j0 = (int64_t)blockIdx.x * W + wic;
-  auto lp_of = [&](int64_t t) -> int64_t { return t < n_list ? (list ? (int64_t)list[t] : t) : -1; };
-  // With the late TMA (NT > 0) the next LP's data is only requested at the
-  // end of the current solve, so one LP of lookahead suffices: the ticket is
-  // claimed when the current solve starts. A deeper pipeline would leave
-  // claimed-but-unstarted LPs behind slow warps at the end of the batch.
-  constexpr int64_t kAhead = L::kLateTma ? 1 : 2;
-  int64_t lpA = lp_of(j0), lpB = L::kLateTma ? -1 : lp_of(j0 + TW);
-  uint32_t hA = load_header_word<T>(p, lpA, lane);  // LP being solved
-  uint32_t hB = L::kLateTma ? 0u : load_header_word<T>(p, lpB, lane);  // LP being staged
-  uint32_t ticket = L::kLateTma ? 0u : atomic_add_if(p.counter, lane == 0);
-  Header<T> h = unpack_header<L, T>(hA, lpA);
-  if (lane == 0 && h.lp >= 0) issue_tma<L, T, P>(p, h, buf, bar, policy);
-  // deferred pair export of the previous LP (lanes 0 and 1)
-  int64_t pend_lp = -1;
-  uint32_t pend_pos = kNone, pend_q = 0;
-
-#ifdef LP2D_PROFILE_WAIT
-  long long prof_wait = 0;
-  const long long prof_t0 = clock64();
-#endif
-  while (h.lp >= 0) {
-    if constexpr (L::kLateTma) ticket = atomic_add_if(p.counter, lane == 0);
-#ifdef LP2D_PROFILE_WAIT
-    const long long tw0 = clock64();
-#endif
-    mbar_wait(bar, phase);
-    phase ^= 1u;
-#ifdef LP2D_PROFILE_WAIT
-    prof_wait += clock64() - tw0;
-#endif
-#ifdef LP2D_PROFILE_TIMELINE
-    uint64_t tl_t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_t0));
-#endif
-
-    // ---- gather: chunk K of the insertion order into registers / the tail --
-    // Out-of-range perm entries are clamped for the load and reported through
-    // pmax (status LP2D_INVALID). sbits tracks max |ax|+|ay| as float bits,
-    // which orders NaN/INF above every finite value.
-    T rax[NS], ray[NS], rb[NS];
-    const int mj = h.ok ? h.m : 0;
-    const int mpos = mj + 4;
-    uint32_t pmax = 0;
-    decltype(float_bits(T(0))) sbits = 0;
-#pragma unroll
-    for (int K = 0; K < NS; ++K) {
-      // Branch-free so the loads of consecutive chunks overlap: every lane
-      // loads (clamped, always in bounds) and padding is selected after.
-      const int P_ = 32 * K + lane;
-      const bool valid = P_ < mpos && !(K == 0 && P_ < 4);
-      const uint32_t o_raw = sperm[K == 0 ? max(P_ - 4, 0) : P_ - 4];
-      const uint32_t o = valid ? o_raw : 0u;
-      pmax = max(pmax, o);
-      const uint32_t oc = min(o, (uint32_t)(L::kCap - 1));
-      // padding positions (>= m+4) never violate: 0*px + 0*py <= +INF
-      T vax = valid ? sax[oc] : T(0);
-      T vay = valid ? say[oc] : T(0);
-      T vb = valid ? sb[oc] : T(INFINITY);
-      if constexpr (NT == 0) sbits = max(sbits, float_bits(fabs(vax) + fabs(vay)));
-      if (K == 0 && P_ < 4) {
-        vax = P_ == 0 ? T(1) : (P_ == 1 ? T(-1) : T(0));
-        vay = P_ == 2 ? T(1) : (P_ == 3 ? T(-1) : T(0));
-        vb = h.M;
-      }
-      rax[K] = vax;
-      ray[K] = vay;
-      rb[K] = vb;
-    }
-    if constexpr (NT > 0) {
-      // Tail: validate the permutation only (read in place later) ...
-#pragma unroll 1
-      for (int c = 0; c < NT && 32 * (NS + c) < mpos; ++c) {
-        const int P_ = 32 * (NS + c) + lane;
-        if (P_ < mpos) pmax = max(pmax, (uint32_t)sperm[P_ - 4]);
-      }
-      // ... and bound max |ax|+|ay| over the whole LP in ORIGINAL order with
-      // 16-byte vector loads (order-independent, conflict-free).
-      constexpr int V = 16 / sizeof(T);
-#pragma unroll 1
-      for (int i = lane * V; i < mj; i += 32 * V) {
-        typedef typename std::conditional<sizeof(T) == 4, float4, double2>::type VecT;
-        const VecT vx = *reinterpret_cast<const VecT*>(sax + i);
-        const VecT vy = *reinterpret_cast<const VecT*>(say + i);
-        const T* xs = reinterpret_cast<const T*>(&vx);
-        const T* ys = reinterpret_cast<const T*>(&vy);
-#pragma unroll
-        for (int e = 0; e < V; ++e)
-          if (i + e < mj) sbits = max(sbits, float_bits(fabs(xs[e]) + fabs(ys[e])));
-      }
-    }
-    const bool bad = !h.ok || (mj > 0 && __reduce_max_sync(kFull, pmax) >= (uint32_t)mj);
-    __syncwarp();
-    fence_proxy_async_smem();
-
-    // ---- advance the pipeline (all inputs were requested an LP ago) --------
-    Header<T> hn;
-    if constexpr (!L::kLateTma) {
-      hn = unpack_header<L, T>(hB, lpB);
-      if (lane == 0 && hn.lp >= 0) issue_tma<L, T, P>(p, hn, buf, bar, policy);
-    }
-    const int64_t tk = (int64_t)__shfl_sync(kFull, ticket, 0) + kAhead * TW;
-    lpB = lp_of(tk);
-    hB = load_header_word<T>(p, lpB, lane);
-    if constexpr (!L::kLateTma) ticket = atomic_add_if(p.counter, lane == 0);
-    if (pend_lp >= 0 && lane < 2 && p.pair) p.pair[2 * pend_lp + lane] = pair_code(pend_pos, pend_q);
-
-    // Per-LP parallel-test bound (see wu_fold), never below the fast
-    // division's divisor floor. LPs outside the proven range go to the exact
-    // global-memory solver.
-    const T m_all = float_from_bits<T>(reduce_max_bits(sbits));
-    bool wild = !(m_all < Limits<T>::kBig) || !(fabs(h.M) < T(INFINITY));
-    const T lpbnd = fmax(fmax(fmax(m_all, T(1)), Limits<T>::kSmall) * eps_hi,
-                         FastDiv<T>::kDLo);
-
-    // ---- solve (serial.hpp:159-188) -----------------------------------------
-    LPState<T> S;
-    lp_init(S, h);
-    S.st = bad ? 255 : 0;
-    const T cthr = eps_par * sqrt(h.cx * h.cx + h.cy * h.cy);
-    int s = 0;                         // chunk where the sweep resumes
-    uint32_t startmask = 0xfffffff0u;  // the box is never tested
-    bool running = !bad && !wild;
-    while (running) {
-      // Speculative chunked violation test from chunk s onward.
-      const T px = S.px, py = S.py;
-      int sfound = -1;
-      uint32_t vfound = 0;
-      T hx = T(0), hy = T(0), hb = T(0);
-      switch (s) {
-        LP2D_TEST_CASE(0) LP2D_TEST_CASE(1) LP2D_TEST_CASE(2) LP2D_TEST_CASE(3)
-        LP2D_TEST_CASE(4) LP2D_TEST_CASE(5) LP2D_TEST_CASE(6) LP2D_TEST_CASE(7)
-        LP2D_TEST_CASE(8) LP2D_TEST_CASE(9) LP2D_TEST_CASE(10) LP2D_TEST_CASE(11)
-        LP2D_TEST_CASE(12) LP2D_TEST_CASE(13) LP2D_TEST_CASE(14) LP2D_TEST_CASE(15)
-        LP2D_TEST_CASE(16) LP2D_TEST_CASE(17) LP2D_TEST_CASE(18) LP2D_TEST_CASE(19)
-        LP2D_TEST_CASE(20) LP2D_TEST_CASE(21) LP2D_TEST_CASE(22) LP2D_TEST_CASE(23)
-        LP2D_TEST_CASE(24) LP2D_TEST_CASE(25) LP2D_TEST_CASE(26) LP2D_TEST_CASE(27)
-        LP2D_TEST_CASE(28) LP2D_TEST_CASE(29) LP2D_TEST_CASE(30) LP2D_TEST_CASE(31)
-        LP2D_TEST_CASE(32) LP2D_TEST_CASE(33) LP2D_TEST_CASE(34) LP2D_TEST_CASE(35)
-        LP2D_TEST_CASE(36) LP2D_TEST_CASE(37) LP2D_TEST_CASE(38) LP2D_TEST_CASE(39)
-        default:
-          // The tail: chunks NS.. from shared memory, rolled.
-          if constexpr (NT > 0) {
-#pragma unroll 1
-            for (int c = (s > NS ? s : NS); c < NS + NT && 32 * c < mpos; ++c) {
-              T qx, qy, qb;
-              tail_load(c - NS, qx, qy, qb);
-              const bool v = (32 * c + lane < mpos) && !satisfied(qx, qy, qb, px, py, eps_feas);
-              const uint32_t vm = __ballot_sync(kFull, v) & startmask;
-              startmask = kFull;
-              if (vm) {
-                hx = qx;
-                hy = qy;
-                hb = qb;
-                vfound = vm;
-                sfound = c;
-                break;
-              }
-            }
-          }
-          break;
-      }
-      if (sfound < 0) break;
-      // Launder the chunk so the work-unit loop below is one shared copy, not
-      // specialised per dispatch exit.
-      s = opaque_int(sfound);
-
-      // Violation at position pi = 4 + i: 1D LP over positions 0..pi-1.
-      // (Copies + one shuffle after the dispatch, not a shuffle per case:
-      // keeps every case a few instructions and the arrays in registers.)
-      const int f = __ffs(vfound) - 1;
-      hx = __shfl_sync(kFull, hx, f);
-      hy = __shfl_sync(kFull, hy, f);
-      hb = __shfl_sync(kFull, hb, f);
-      const uint32_t pi = 32u * (uint32_t)s + (uint32_t)f;
-      S.viol += 1;
-      S.wu += pi;  // considered.size() (serial.hpp:176-179)
-      const Line<T> l = boundary_of(hx, hy, hb);
-      Acc<T> acc;
-      acc.uL = -T(INFINITY);
-      acc.uR = T(INFINITY);
-      acc.oL = acc.oR = acc.par = kNone;
-      bool rare = false;
-      const int rel = (int)pi - lane;  // position 32*K + lane < pi  <=>  32*K < rel
-      // Chunks are folded in pairs between exit checks, so the division
-      // chains of a pair overlap (a chunk past s is fully masked). Owners are
-      // recorded as chunk indices (immediates) and turned into positions after.
-#pragma unroll
-      for (int K = 0; K < NS; ++K) {
-        wu_fold(rax[K], ray[K], rb[K], l, lpbnd, (uint32_t)K, 32 * K < rel, acc, rare);
-        if ((K % kWuGroup == kWuGroup - 1) && K >= s) break;
-      }
-      if constexpr (NT > 0) {
-#pragma unroll 1
-        for (int c = NS; c <= s; c += 2) {
-          T x0, y0, b0, x1, y1, b1;
-          tail_load(c - NS, x0, y0, b0);
-          tail_load(min(c + 1, NS + NT - 1) - NS, x1, y1, b1);
-          wu_fold(x0, y0, b0, l, lpbnd, (uint32_t)c, 32 * c < rel, acc, rare);
-          wu_fold(x1, y1, b1, l, lpbnd, (uint32_t)(c + 1), 32 * (c + 1) < rel, acc, rare);
-        }
-      }
-      acc.oL = acc.oL == kNone ? kNone : ((acc.oL << 5) | (uint32_t)lane);
-      acc.oR = acc.oR == kNone ? kNone : ((acc.oR << 5) | (uint32_t)lane);
-      const bool rare_any = __any_sync(kFull, rare);
-      Merged<T> mg = merge_lanes(acc, false);
-      if (rare_any) {
-        acc = fold_exact_global<T, P>(p, h.off, pi, l, h.M, eps_par, eps_feas, eps_hi);
-        mg = merge_lanes(acc, true);
-      }
-      if (!resolve_merged(S, mg, l, pi, h, cthr, eps_feas)) break;
-      if (!(fabs(S.px) < T(INFINITY) && fabs(S.py) < T(INFINITY))) {
-        wild = true;  // the padding test needs a finite optimum
-        break;
-      }
-      if (f == 31) {
-        s += 1;
-        startmask = kFull;
-      } else {
-        startmask = kFull << (f + 1);
-      }
-    }
-    if (wild && !bad) solve_exact_global<T, P>(p, h, eps_par, eps_feas, eps_hi, S);
-    if constexpr (L::kLateTma) {  // the tail lived in the staging buffer until now
-      __syncwarp();
-      fence_proxy_async_smem();
-      hn = unpack_header<L, T>(hB, lpB);
-      if (lane == 0 && hn.lp >= 0) issue_tma<L, T, P>(p, hn, buf, bar, policy);
-    }
-    uint8_t st = S.st;
-    if (st == 0 && (S.pos0 < 4 || S.pos1 < 4)) st = 2;
-    if (lane == 0) write_main(p, h, st, S.px, S.py, S.viol, S.wu);
-#ifdef LP2D_PROFILE_TIMELINE
-    if (lane == 0) {  // debug: per LP (start ns low 40 bits << 24 | duration ns), SM id
-      uint64_t tl_t1;
-      uint32_t smid;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_t1));
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      const uint64_t d = min(tl_t1 - tl_t0, (uint64_t)0xffffff);
-      p.wu[h.lp] = ((tl_t0 & 0xffffffffffull) << 24) | d;
-      p.viol[h.lp] = (smid << 16) | (uint32_t)(blockIdx.x * W + wic) % 65536u;
-    }
-#endif
-    // pair export: lanes 0/1 request perm[pos-4] now, store one LP later
-    pend_lp = h.lp;
-    pend_pos = lane == 0 ? S.pos0 : S.pos1;
-    if (st == 255) pend_pos = kNone;
-    {
-      const bool need = lane < 2 && pend_pos != kNone && pend_pos >= 4;
-      const P* pa = static_cast<const P*>(p.perm) + h.off + (need ? pend_pos - 4 : 0);
-      pend_q = sizeof(P) == 2 ? ldg_u16_if(pa, need) : ldg_u32_if(pa, need);
-    }
-    h = hn;
-  }
-  if (pend_lp >= 0 && lane < 2 && p.pair) p.pair[2 * pend_lp + lane] = pair_code(pend_pos, pend_q);
-
-#ifdef LP2D_PROFILE_WAIT
-  if (lane == 0 && p.wu) {  // debug: per-warp [wait cycles, total cycles] into wu[]
-    const int64_t gw = (int64_t)blockIdx.x * W + wic;
-    atomicAdd((unsigned long long*)&p.wu[0], (unsigned long long)prof_wait);
-    atomicAdd((unsigned long long*)&p.wu[1], (unsigned long long)(clock64() - prof_t0));
-    (void)gw;
-  }
-#endif
-  // Self-reset of the ticket counter by the last warp to finish, so the next
-  // launch on this counter slot starts from zero without a memset.
-  if (lane == 0) {
-    __threadfence();
-    const uint32_t t = atomicAdd(p.counter + 1, 1u);
-    if (t == (uint32_t)p.total_warps - 1) {
-      p.counter[0] = 0;
-      p.counter[1] = 0;
-    }
-  }
-}
-#undef LP2D_TEST_CASE
+// k_solve_warp (the balanced warp-per-LP solver) lives in lp2d_warp.cuh.
 
 // Naive: thread per LP, the serial loop with global-memory gathers.
 template <typename T, typename P>
@@ -1589,3 +1250,5 @@ __global__ void k_shuffle(int64_t n, const int32_t* m, const int64_t* offset,
 }
 
 }  // namespace lp2d_b200
+
+#include "lp2d_warp.cuh"
