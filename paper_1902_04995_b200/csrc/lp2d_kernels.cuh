@@ -507,7 +507,7 @@ __device__ __noinline__ void solve_exact_global(const KParams& p, const Header<T
 
 // Naive: thread per LP, the serial loop with global-memory gathers.
 template <typename T, typename P>
-__global__ void __launch_bounds__(128) k_solve_naive(const KParams p) {
+__global__ void __launch_bounds__(128) k_solve_naive(const __grid_constant__ KParams p) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int32_t* list;
   int64_t n_list;
@@ -641,7 +641,7 @@ __device__ __forceinline__ Line<T> shfl_line(const Line<T>& l, int src) {
 }
 
 template <typename T, typename P, int MAXM>
-__global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const KParams p) {
+__global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid_constant__ KParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   using LT = LaneTile<T, MAXM>;
   constexpr int ST = LT::kStride;
@@ -892,7 +892,7 @@ __device__ __forceinline__ Header<T> unpack_header_cap(uint32_t w, int64_t lp, i
 }
 
 template <typename T, typename P, int THREADS>
-__global__ void __launch_bounds__(THREADS) k_solve_cta(const KParams p, int32_t cap) {
+__global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ KParams p, int32_t cap) {
   static_assert(sizeof(T) == 4 || sizeof(T) == 8, "scalar");
   constexpr int W = THREADS / 32;
   static_assert(W <= kCtaMaxWarps, "warps per CTA");
@@ -1107,7 +1107,7 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const KParams p, int32_t 
 // Large LPs (m above the register classes) and any other LP: one warp per
 // LP straight from global memory (solve_exact_global), claimed dynamically.
 template <typename T, typename P>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_solve_global(const KParams p) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_solve_global(const __grid_constant__ KParams p) {
   const int lane = threadIdx.x & 31;
   const int32_t* list;
   int64_t n_list;
