@@ -194,8 +194,8 @@ __device__ __forceinline__ uint32_t ldg_u32_if(const void* addr, bool pred) {
 __device__ __forceinline__ uint32_t ldg_u16_if(const void* addr, bool pred) {
   uint32_t v = 0;
   asm volatile(
-      "{\n\t.reg .pred q;\n\t.reg .u16 t;\n\tsetp.ne.u32 q, %2, 0;\n\t"
-      "@q ld.global.nc.u16 t, [%1];\n\t@q cvt.u32.u16 %0, t;\n\t}"
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+      "@q ld.global.nc.u16 %0, [%1];\n\t}"
       : "+r"(v)
       : "l"(addr), "r"((uint32_t)pred)
       : "memory");
