@@ -129,12 +129,19 @@ int launch_warp_kernel(KParams kp, int dev, cudaStream_t stream) {
   constexpr int kWarpsPerCta = L::kWarps;
   auto kern = k_solve_warp<T, P, NS, NT>;
   static int blocks_per_sm[64] = {0};
+  // (experiment knob: LP2D_B200_SMEM_PAD bytes of extra shared memory per CTA
+  // lower the resident warps, for occupancy-sensitivity measurements)
+  static const size_t pad = [] {
+    const char* e = std::getenv("LP2D_B200_SMEM_PAD");
+    return e ? (size_t)std::atol(e) : (size_t)0;
+  }();
+  const size_t smem = L::kSmem + pad;
   if (!blocks_per_sm[dev]) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)L::kSmem));
+                                  (int)smem));
     int b = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kWarpsPerCta * 32,
-                                                           L::kSmem));
+                                                           smem));
     if (b < 1) return fail(LP2D_ERR_CUDA, "warp kernel does not fit on an SM");
     blocks_per_sm[dev] = b;
   }
@@ -143,7 +150,7 @@ int launch_warp_kernel(KParams kp, int dev, cudaStream_t stream) {
   const int grid = (int)std::max<int64_t>(1, std::min(want, maxb));
   kp.total_warps = grid * kWarpsPerCta;
   kp.counter = take_counter(dev);
-  kern<<<grid, kWarpsPerCta * 32, L::kSmem, stream>>>(kp);
+  kern<<<grid, kWarpsPerCta * 32, smem, stream>>>(kp);
   note_launch();
   CUDA_TRY(cudaGetLastError());
   return 0;

@@ -111,10 +111,12 @@ struct WarpLayout {
 #ifndef LP2D_MIN_BLOCKS
 #define LP2D_MIN_BLOCKS 3
 #endif
+#ifndef LP2D_MIN_BLOCKS_F64
+#define LP2D_MIN_BLOCKS_F64 3
+#endif
+  static constexpr int kMinB = sizeof(T) == 8 ? LP2D_MIN_BLOCKS_F64 : LP2D_MIN_BLOCKS;
   static constexpr int kMinBlocks =
-      blocks_for(kWarps) < 1 ? 1
-                             : (blocks_for(kWarps) < LP2D_MIN_BLOCKS ? blocks_for(kWarps)
-                                                                     : LP2D_MIN_BLOCKS);
+      blocks_for(kWarps) < 1 ? 1 : (blocks_for(kWarps) < kMinB ? blocks_for(kWarps) : kMinB);
   static constexpr uint32_t kSmem = kWarps * kBuf + kWarps * 8;
   // Register chunks below this index are never past the end of an LP of this
   // size class (m + 4 > 32 * previous class's chunks), so their test needs
