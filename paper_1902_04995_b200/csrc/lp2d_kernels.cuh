@@ -109,7 +109,7 @@ struct WarpLayout {
   static constexpr int kWarps =
       (blocks_for(5) * 5 > blocks_for(4) * 4 && blocks_for(5) >= 1) ? 5 : 4;
 #ifndef LP2D_MIN_BLOCKS
-#define LP2D_MIN_BLOCKS 3
+#define LP2D_MIN_BLOCKS 4
 #endif
 #ifndef LP2D_MIN_BLOCKS_F64
 #define LP2D_MIN_BLOCKS_F64 3
