@@ -265,7 +265,10 @@ int launch_cta_kernel(KParams kp, int64_t max_m, int dev, cudaStream_t stream) {
 
 template <typename T, typename P>
 int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t max_m) {
-  if (cls >= n_reg_classes<T>()) return launch_cta_kernel<T, P>(kp, max_m, dev, s);
+  // (experiment knob: LP2D_B200_FORCE_CTA=1 sends every class to the CTA kernel)
+  static const bool force_cta = std::getenv("LP2D_B200_FORCE_CTA") &&
+                                std::getenv("LP2D_B200_FORCE_CTA")[0] == '1';
+  if (cls >= n_reg_classes<T>() || force_cta) return launch_cta_kernel<T, P>(kp, max_m, dev, s);
   switch (kSlotClasses[cls]) {
     case 1:
       if (tiny_uses_lanes()) return launch_lane_kernel<T, P>(kp, dev, s);

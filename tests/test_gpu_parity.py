@@ -310,3 +310,45 @@ def test_cpp_drop_in_against_reference_headers():
         pytest.skip("shim_test not built (needs the reference headers)")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_adversarial_inputs_every_warp_class(P, O, dt):
+    """Every warp-kernel size class (register classes, the register+tail
+    class) under inputs that defeat each fast-path shortcut and must take the
+    exact reference operations instead: duplicated and parallel constraints
+    (parallel-bound refolds), huge coefficients (infinite per-lane bound),
+    tiny right-hand sides (line through the fast sqrt/div range check),
+    zero normals (NaN lines), NaN and infinite entries. Bit-identical to the
+    oracle in both precisions."""
+    rng = np.random.default_rng(21)
+    sizes = np.array([40, 100, 150, 300, 500, 700, 1000] * 6, np.int32)
+    pb = P.PackedBatch.generate(sizes, 77).astype(dt)
+    ax, ay, b = pb.ax, pb.ay, pb.b
+    for j in range(pb.n):
+        o, mj = int(pb.offset[j]), int(pb.m[j])
+        sel = j % 6
+        k = rng.integers(0, mj, 8)
+        if sel == 0:    # duplicates and scaled (parallel) copies
+            src = rng.integers(0, mj, 8)
+            ax[o + k], ay[o + k], b[o + k] = ax[o + src], ay[o + src], b[o + src]
+            ax[o + k[:4]] *= dt(2)
+            ay[o + k[:4]] *= dt(2)
+            b[o + k[:4]] *= dt(2)
+        elif sel == 1:  # huge coefficients, late in the permutation too
+            ax[o + k] *= dt(1e20) if dt == np.float32 else dt(1e160)
+        elif sel == 2:  # tiny right-hand sides
+            b[o + k] *= dt(1e-30) if dt == np.float32 else dt(1e-300)
+        elif sel == 3:  # zero normals, violated (b < 0) or not
+            ax[o + k] = 0
+            ay[o + k] = 0
+            b[o + k[:4]] = -1
+        elif sel == 4:  # NaN entry
+            ay[o + k[0]] = np.nan
+        else:           # infinite right-hand sides and nearly parallel pairs
+            b[o + k[:3]] = np.inf
+            ax[o + k[3:]] = ax[o + k[2]] * (dt(1) + dt(2) ** -20)
+            ay[o + k[3:]] = ay[o + k[2]]
+    o = O.solve_batch(pb)
+    for sched in SCHEDS:
+        assert_same_as_oracle(P.solve_packed(pb, _cfg(P, sched)), o, O, f"adversarial {sched}")
