@@ -138,6 +138,24 @@ int lp2dgpu_shuffle_device(int64_t n, const int32_t* m, const int64_t* offset,
                            const uint64_t* seeds, void* perm, int32_t perm_bits,
                            int32_t device, void* stream);
 
+/* Device-side instance synthesis (replaces the host
+ * path of lp2d::gen_mixed, /root/reference/proj/include/lp2d/generate.hpp:
+ * 60-91, 174-189, for batches that should not cross PCIe). LP j (global index
+ * g = first + j) is gen({m[j], derive_seed(seed, 2g), kind[j], margin}) with
+ * insertion order shuffle(m[j], derive_seed(seed, 2g+1)), written in the
+ * packed layout at offset[j]; b and bound_m scaled by bscale. kind as in
+ * lp2d_b200_gen.h (NULL: all feasible; an infeasible LP needs m >= 1, else it
+ * is generated feasible). The integer streams (seeds, draws, permutations)
+ * are bit-identical to lp2dgen_fill; cos/sin are the device's (an ulp or two
+ * from glibc's). scalar_bits 32 stores the fp64 instance rounded to float
+ * (as lp2dgen_fill + a cast). perm may be NULL. Device pointers, enqueued on
+ * stream. */
+int lp2dgpu_generate_device(int64_t n, int64_t first, uint64_t seed, const int32_t* m,
+                            const int64_t* offset, const uint8_t* kind, double margin,
+                            double bscale, int32_t scalar_bits, void* ax, void* ay, void* b,
+                            void* perm, int32_t perm_bits, void* c, void* bound_m,
+                            int32_t device, void* stream);
+
 /* ---- contention microbenchmark -------------------
  * Segmented extremes: out_min[g] / out_max[g] = min / max of the g-th
  * consecutive group of `contention` values of in[0..n) — replaces

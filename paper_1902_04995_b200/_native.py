@@ -86,6 +86,7 @@ EXPORTS = (
     "lp2dgpu_pack_offsets",
     "lp2dgpu_partition",
     "lp2dgpu_shuffle_device",
+    "lp2dgpu_generate_device",
     "lp2dgpu_device_count",
     "lp2dgpu_kernel_launches",
     "lp2dgpu_segmented_extremes",
@@ -132,6 +133,12 @@ def lib():
     L.lp2dgpu_shuffle_device.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
     L.lp2dgpu_shuffle_device.restype = C.c_int
+    L.lp2dgpu_generate_device.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                                          C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                          C.c_int32, C.c_void_p]
+    L.lp2dgpu_generate_device.restype = C.c_int
     L.lp2dgpu_device_count.restype = C.c_int
     L.lp2dgpu_kernel_launches.restype = C.c_uint64
     L.lp2dgpu_segmented_extremes.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int32,

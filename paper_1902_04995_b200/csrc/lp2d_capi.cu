@@ -658,6 +658,43 @@ int lp2dgpu_shuffle_device(int64_t n, const int32_t* m, const int64_t* offset,
   return 0;
 }
 
+int lp2dgpu_generate_device(int64_t n, int64_t first, uint64_t seed, const int32_t* m,
+                            const int64_t* offset, const uint8_t* kind, double margin,
+                            double bscale, int32_t scalar_bits, void* ax, void* ay, void* b,
+                            void* perm, int32_t perm_bits, void* c, void* bound_m,
+                            int32_t device, void* stream) {
+  if (n < 0) return fail(LP2D_ERR_ARG, "generate: negative count");
+  if (n == 0) return 0;
+  if (!m || !offset || !ax || !ay || !b || !c || !bound_m)
+    return fail(LP2D_ERR_ARG, "generate: null argument");
+  if (scalar_bits != 32 && scalar_bits != 64)
+    return fail(LP2D_ERR_ARG, "generate: scalar_bits must be 32 or 64");
+  if (perm && perm_bits != 16 && perm_bits != 32)
+    return fail(LP2D_ERR_ARG, "generate: perm_bits must be 16 or 32");
+  DeviceGuard guard;
+  if (int rc = ensure_device(device)) return rc;
+  CUDA_TRY(cudaSetDevice(device));
+  const int threads = 64;
+  const unsigned grid = (unsigned)((n + threads - 1) / threads);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto go = [&](auto tag_t, auto tag_p) {
+    using T = decltype(tag_t);
+    using Pt = decltype(tag_p);
+    k_generate<T, Pt><<<grid, threads, 0, s>>>(
+        n, first, seed, m, offset, kind, margin, bscale, static_cast<T*>(ax), static_cast<T*>(ay),
+        static_cast<T*>(b), static_cast<Pt*>(perm), static_cast<T*>(c), static_cast<T*>(bound_m));
+  };
+  const bool p16 = perm_bits == 16;
+  if (scalar_bits == 32) {
+    if (p16) go(float(), uint16_t()); else go(float(), uint32_t());
+  } else {
+    if (p16) go(double(), uint16_t()); else go(double(), uint32_t());
+  }
+  note_launch();
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 int lp2dgpu_segmented_extremes(const double* in, int64_t n, int64_t contention, int32_t strategy,
                                double* out_min, double* out_max, int32_t device, void* stream) {
   // reduction.hpp:52-64 validation, as codes

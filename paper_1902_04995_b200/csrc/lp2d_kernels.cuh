@@ -1251,6 +1251,80 @@ __global__ void k_shuffle(int64_t n, const int32_t* m, const int64_t* offset,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Device-side instance synthesis: generate.hpp:60-91
+// (feasible_random, infeasible) plus the builder's unbounded kind, LP j of
+// global index g = first + j seeded derive_seed(seed, 2g) and its insertion
+// order shuffle(m, derive_seed(seed, 2g+1)) — lp2d::gen_mixed streams,
+// generate.hpp:174-189. Integer parts (seeds, draws, permutations) are
+// bit-identical to the host generator; cos/sin are CUDA's (within an ulp or
+// two of glibc's), so parity of a solve over a device-generated batch is
+// checked against the oracle on the DOWNLOADED instance. One thread per LP
+// (the per-LP draw stream is sequential); scalars stored as T.
+__device__ __forceinline__ uint64_t derive_seed_dev(uint64_t base, uint64_t stream) {
+  uint64_t st = base ^ (0x9e3779b97f4a7c15ull * (stream + 1));  // rng.hpp:64-68
+  splitmix64(st);
+  return splitmix64(st);
+}
+
+__device__ __forceinline__ double unit_dev(Xoshiro& r) {  // rng.hpp:39-41
+  return (double)(r.next() >> 11) * 0x1.0p-53;
+}
+
+template <typename T, typename P>
+__global__ void k_generate(int64_t n, int64_t first, uint64_t seed, const int32_t* m,
+                           const int64_t* offset, const uint8_t* kind, double margin,
+                           double bscale, T* ax, T* ay, T* b, P* perm, T* c, T* bound_m) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  constexpr double kTwoPi = 6.283185307179586;
+  constexpr double kPi = 3.141592653589793;
+  constexpr double kBound = 1e7;  // serial.hpp:26 default bound_m
+  const uint64_t g = (uint64_t)(first + j);
+  const int32_t mj = m[j];
+  const int64_t o = offset[j];
+  const int kd = kind ? (int)kind[j] : 0;
+  Xoshiro r(derive_seed_dev(seed, 2 * g));
+  // feasible_random core (generate.hpp:60-79) over mf constraints
+  const int64_t mf = (kd == 1 && mj >= 1) ? mj - 1 : mj;
+  const double phi = kTwoPi * unit_dev(r);
+  c[2 * j] = (T)cos(phi);
+  c[2 * j + 1] = (T)sin(phi);
+  const double half = kBound / 2.0;
+  const double ix = -half + (half - -half) * unit_dev(r);  // rng.hpp:42 in_range
+  const double iy = -half + (half - -half) * unit_dev(r);
+  for (int64_t k = 0; k < mf; ++k) {
+    double theta = kTwoPi * unit_dev(r);
+    if (kd == 3)  // builder-defined unbounded kind: theta in (phi + pi) +- pi/3
+      theta = phi + kPi + (theta / kTwoPi * 2.0 - 1.0) * (kPi / 3.0);
+    const double a0 = cos(theta), a1 = sin(theta);
+    const double slack = margin * (1.0 + 9.0 * unit_dev(r));
+    ax[o + k] = (T)a0;
+    ay[o + k] = (T)a1;
+    b[o + k] = (T)(((a0 * ix + a1 * iy) + slack) * bscale);
+  }
+  if (kd == 1 && mj >= 1) {  // generate.hpp:81-91: one constraint excluding the box
+    const double theta = kTwoPi * unit_dev(r);
+    const double a0 = cos(theta), a1 = sin(theta);
+    const double box_min = -(fabs(a0) + fabs(a1)) * kBound;
+    ax[o + mj - 1] = (T)a0;
+    ay[o + mj - 1] = (T)a1;
+    b[o + mj - 1] = (T)((box_min - 1.0) * bscale);
+  }
+  bound_m[j] = (T)(kBound * bscale);
+  if (perm) {  // serial.hpp:138-146 shuffle
+    P* q = perm + o;
+    for (int32_t i = 0; i < mj; ++i) q[i] = (P)i;
+    Xoshiro s(derive_seed_dev(seed, 2 * g + 1));
+    for (int64_t i = mj; i > 1; --i) {
+      const uint64_t t = s.below((uint64_t)i);
+      const P tmp = q[i - 1];
+      q[i - 1] = q[t];
+      q[t] = tmp;
+    }
+  }
+}
+
 }  // namespace lp2d_b200
 
 #include "lp2d_warp.cuh"

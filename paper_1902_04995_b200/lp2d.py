@@ -393,6 +393,59 @@ class DeviceBatch:
         self.c, self.M = t(pb.c), t(pb.M)
         self.constraint_bytes = pb.constraint_bytes()
 
+    @classmethod
+    def generate(cls, m: Sequence[int], seed: int, kind=None, margin: float = 1.0,
+                 bscale: float = 1.0, first: int = 0, dtype=np.float64,
+                 perm_bits: Optional[int] = None, device: int = 0,
+                 stream=None) -> "DeviceBatch":
+        """PackedBatch.generate on the GPU (lp2dgpu_generate_device): the same
+        streams, synthesized in HBM (no host arrays, no PCIe)."""
+        import torch
+
+        dev = torch.device("cuda", device)
+        m = np.ascontiguousarray(m, dtype=np.int32)
+        n = len(m)
+        off = pack_offsets(m)
+        E = int(off[-1])
+        if perm_bits is None:
+            perm_bits = 16 if m.max(initial=0) <= 65536 else 32
+        tdt = torch.float32 if dtype == np.float32 else torch.float64
+        self = cls.__new__(cls)
+        self.n, self.device, self.dtype = n, device, np.dtype(dtype).type
+        self.max_m = int(m.max(initial=0))
+        self.min_m = int(m.min()) if n else 0
+        self.m = torch.from_numpy(m).to(dev)
+        self.offset = torch.from_numpy(off).to(dev)
+        self.ax = torch.zeros(E, dtype=tdt, device=dev)
+        self.ay = torch.zeros(E, dtype=tdt, device=dev)
+        self.b = torch.zeros(E, dtype=tdt, device=dev)
+        self.perm = torch.zeros(E, dtype=torch.int16 if perm_bits == 16 else torch.int32, device=dev)
+        self.perm_bits = perm_bits
+        self.c = torch.zeros(2 * n, dtype=tdt, device=dev)
+        self.M = torch.zeros(n, dtype=tdt, device=dev)
+        kd = None
+        if kind is not None:
+            kd = torch.from_numpy(np.broadcast_to(np.asarray(kind, dtype=np.uint8), (n,)).copy()).to(dev)
+        self.constraint_bytes = 3 * int(m.astype(np.int64).sum()) * (4 if dtype == np.float32 else 8)
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        rc = N.lib().lp2dgpu_generate_device(
+            n, first, seed & (2**64 - 1), self.m.data_ptr(), self.offset.data_ptr(),
+            kd.data_ptr() if kd is not None else None, margin, bscale,
+            32 if dtype == np.float32 else 64, self.ax.data_ptr(), self.ay.data_ptr(),
+            self.b.data_ptr(), self.perm.data_ptr(), perm_bits, self.c.data_ptr(),
+            self.M.data_ptr(), device, stream.cuda_stream)
+        if rc:
+            _raise(rc)
+        return self
+
+    def to_packed(self) -> PackedBatch:
+        """Download (e.g. to check a device-generated batch on the oracle)."""
+        np_ = lambda t: t.cpu().numpy()
+        perm = np_(self.perm).view(np.uint16 if self.perm_bits == 16 else np.uint32)
+        return PackedBatch(np_(self.m), np_(self.offset), np_(self.ax), np_(self.ay), np_(self.b),
+                           perm, np_(self.c), np_(self.M))
+
     def empty_result(self) -> PackedResult:
         import torch
 

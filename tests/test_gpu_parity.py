@@ -352,3 +352,38 @@ def test_adversarial_inputs_every_warp_class(P, O, dt):
     o = O.solve_batch(pb)
     for sched in SCHEDS:
         assert_same_as_oracle(P.solve_packed(pb, _cfg(P, sched)), o, O, f"adversarial {sched}")
+
+
+def test_device_generator_streams_and_parity(P, O):
+    """lp2dgpu_generate_device: the integer streams
+    (permutations, and hence every draw) are bit-identical to the host
+    generator; the trigonometry is the device's, within a few ulps of glibc;
+    a solve over the device-generated batch is bit-identical to the oracle
+    run on the downloaded instance (fp64 and fp32, all kinds)."""
+    rng = np.random.default_rng(3)
+    m = rng.integers(1, 1100, 600).astype(np.int32)
+    kind = rng.choice([P.GenKind.feasible_random, P.GenKind.infeasible,
+                       P.GenKind.unbounded_random], 600).astype(np.uint8)
+    host = P.PackedBatch.generate(m, 99, kind=kind, first=7)
+    for dt in (np.float64, np.float32):
+        db = P.DeviceBatch.generate(m, 99, kind=kind, first=7, dtype=dt)
+        dv = db.to_packed()
+        assert np.array_equal(dv.perm, host.perm)
+        assert np.array_equal(dv.offset, host.offset)
+        hx = host.astype(dt)
+        eps = np.finfo(dt).eps
+        for a, h in ((dv.ax, hx.ax), (dv.ay, hx.ay), (dv.c, hx.c)):  # unit vectors
+            assert np.allclose(a, h, rtol=0, atol=4 * eps)
+        # b = a.interior + slack with |interior| <= 5e6: a 1-ulp cos/sin
+        # difference moves b by <= ~1e7 ulps of 1 (then float rounding)
+        assert np.allclose(dv.b, hx.b, rtol=0, atol=1e7 * 8 * np.finfo(np.float64).eps + 2 * eps * 1.5e7)
+        assert np.array_equal(dv.M, hx.M)
+        out = db.empty_result()
+        P.solve_device(db, out)
+        o = O.solve_batch(dv)
+        st = out.status.cpu().numpy().astype(np.int32)
+        assert np.array_equal(st, o["status"])
+        assert np.array_equal(out.pair.cpu().numpy(), o["pair"])
+        feas = o["status"] != O.INFEASIBLE
+        assert np.array_equal(out.x.cpu().numpy()[feas].astype(np.float64), o["x"][feas])
+        assert np.array_equal(out.work_units.cpu().numpy().astype(np.uint64), o["work_units"])
