@@ -26,6 +26,7 @@
 
 #include "lp2d_device.cuh"
 #include "lp2d_pair.cuh"
+#include "lp2d_fold.cuh"
 
 namespace lp2d_b200 {
 
@@ -1037,18 +1038,40 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
       S.wu += (uint32_t)pi;
       T hx, hy, hb;
       pos(pi, h.M, hx, hy, hb);
-      const Line<T> l = boundary_of(hx, hy, hb);
-      Acc<T> acc;
-      acc.uL = -T(INFINITY);
-      acc.uR = T(INFINITY);
-      acc.oL = acc.oR = acc.par = kNone;
-      bool rare = false;
-#pragma unroll 2
-      for (int k = tid; k < pi; k += THREADS) {
-        T x, y, bb;
-        pos(k, h.M, x, y, bb);
-        wu_fold(x, y, bb, l, lpbnd, (uint32_t)k, true, acc, rare);
+      const Line<T> l = boundary_fast(hx, hy, hb);
+      // The thread's units k = tid + i*THREADS, two per packed fold (k,
+      // k + THREADS), owners = positions; the same range trackers as the
+      // warp kernel certify the fast arithmetic against the per-LP bound.
+      LineP<T> lpair;
+      lpair.ox = splat2(l.ox);
+      lpair.oy = splat2(l.oy);
+      lpair.dx = splat2(l.dx);
+      lpair.dy = splat2(l.dy);
+      FoldAcc<T> fa;
+      acc_init(fa);
+      fa.lbv = lpbnd;
+      int k = tid;
+#pragma unroll 1
+      for (; k + THREADS < pi; k += 2 * THREADS) {
+        T x0, y0, b0, x1, y1, b1;
+        pos(k, h.M, x0, y0, b0);
+        pos(k + THREADS, h.M, x1, y1, b1);
+        fold2s<T, false>(mk2(x0, x1), mk2(y0, y1), mk2(b0, b1), lpair, (uint32_t)k,
+                         (uint32_t)(k + THREADS), true, true, fa, p.pk);
       }
+      if (k < pi) {
+        T x0, y0, b0;
+        pos(k, h.M, x0, y0, b0);
+        fold2s<T, true>(mk2(x0, x0), mk2(y0, y0), mk2(b0, b0), lpair, (uint32_t)k, kNone, true,
+                        false, fa, p.pk);
+      }
+      Acc<T> acc;
+      acc.uL = fa.uL;
+      acc.uR = fa.uR;
+      acc.oL = fa.oL;
+      acc.oR = fa.oR;
+      acc.par = kNone;
+      const bool rare = !FastRange<T>::ok(fa, lpbnd);
       if (__syncthreads_or(rare)) {  // exact reference classify for every unit (rare)
         acc.uL = -T(INFINITY);
         acc.uR = T(INFINITY);
