@@ -107,11 +107,11 @@ uint32_t* take_counter(int dev) {
 }
 
 // Register slot classes: NS slots hold m + 4 positions (box included).
-constexpr int kSlotClasses[] = {1, 2, 4, 6, 10, 18, 33};
+constexpr int kSlotClasses[] = {1, 2, 4, 6, 10, 18, 33, 65};
 
 template <typename T>
 constexpr int max_nslot() {
-  return sizeof(T) == 4 ? 33 : 18;  // fp64 keeps m <= 572 in registers
+  return sizeof(T) == 4 ? 65 : 18;  // fp64 keeps m <= 572 in registers
 }
 
 // Eps_par rounded up by 2^-10 (relative), in T: the parallel-filter factor.
@@ -280,6 +280,9 @@ int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t ma
     case 18: return launch_warp_kernel<T, P, 18>(kp, dev, s);
     case 33:  // 16 register chunks + 17 shared-memory tail chunks
       if constexpr (max_nslot<T>() >= 33) return launch_warp_kernel<T, P, 16, 17>(kp, dev, s);
+      break;
+    case 65:  // 16 register chunks + 49 tail chunks (m <= 2076, 29 KB per warp)
+      if constexpr (max_nslot<T>() >= 65) return launch_warp_kernel<T, P, 16, 49>(kp, dev, s);
       break;
   }
   return fail(LP2D_ERR_UNSUPPORTED, "size class not built");

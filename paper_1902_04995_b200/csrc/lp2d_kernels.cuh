@@ -105,10 +105,17 @@ struct WarpLayout {
   // keeps the big class at 14.7 KB of shared memory per warp (15 warps/SM).
   static constexpr bool kLateTma = NT > 0;
   static constexpr uint32_t kBuf = kStage;  // per warp
-  // Warps per CTA (4 or 5) maximising resident warps under 227 KB of smem.
+  // Warps per CTA maximising resident warps under 227 KB of smem (ties to
+  // the smaller CTA): 4 or 5 for the register-only classes, up to 7 for the
+  // tail classes whose staging buffers bound the CTAs per SM.
   static constexpr int blocks_for(int w) { return (int)((227u * 1024u) / (w * kBuf + w * 8u)); }
-  static constexpr int kWarps =
-      (blocks_for(5) * 5 > blocks_for(4) * 4 && blocks_for(5) >= 1) ? 5 : 4;
+  static constexpr int best_warps() {
+    int bw = 4;
+    for (int w = 5; w <= (NT > 0 ? 7 : 5); ++w)
+      if (blocks_for(w) * w > blocks_for(bw) * bw) bw = w;
+    return bw;
+  }
+  static constexpr int kWarps = best_warps();
 #ifndef LP2D_MIN_BLOCKS
 #define LP2D_MIN_BLOCKS 4
 #endif
