@@ -359,19 +359,37 @@ int launch_balanced(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStrea
     DeviceState& d = g_dev[dev];
     std::lock_guard<std::mutex> lock(d.fork_mu);
     CUDA_TRY(cudaEventRecord(d.cls_event[16], s));
-    for (int c = cmax; c >= cmin && rc == 0; --c) {
-      if (may_sync && host_counts[c] == 0) continue;
+    // The large (CTA) class is launched in two capacity tiers: LPs up to
+    // kCtaTierM share an SM three at a time (57 KB each), only the larger
+    // ones get the whole-batch capacity (up to one LP per SM).
+    constexpr int kTierBins = 8;  // bins holding m < cta_lo + 8 * cta_width
+    const int64_t tier_m = (int64_t)spec.cta_lo + kTierBins * spec.cta_width - 1;
+    auto launch_one = [&](int c, int lo, int hi, int64_t n_host, int64_t cap_m, int sidx) {
       KParams kc = kp;
-      int lo, hi;
-      bin_range(c, lo, hi);
       kc.bin_lo = lo;
       kc.bin_hi = hi;
-      if (may_sync) kc.n_list = host_counts[c];
-      cudaStream_t cs = d.cls_stream[c];
+      if (may_sync) kc.n_list = n_host;
+      cudaStream_t cs = d.cls_stream[sidx];
       CUDA_TRY(cudaStreamWaitEvent(cs, d.cls_event[16], 0));
-      rc = launch_class<T, P>(kc, c, dev, cs, max_m);
-      CUDA_TRY(cudaEventRecord(d.cls_event[c], cs));
-      CUDA_TRY(cudaStreamWaitEvent(s, d.cls_event[c], 0));
+      int r = launch_class<T, P>(kc, c, dev, cs, cap_m);
+      CUDA_TRY(cudaEventRecord(d.cls_event[sidx], cs));
+      CUDA_TRY(cudaStreamWaitEvent(s, d.cls_event[sidx], 0));
+      return r;
+    };
+    for (int c = cmax; c >= cmin && rc == 0; --c) {
+      if (may_sync && host_counts[c] == 0) continue;
+      int lo, hi;
+      bin_range(c, lo, hi);
+      if (c == spec.nreg && max_m > tier_m) {
+        const int mid = hi - kTierBins;
+        int64_t n_big = 0, n_small = 0;
+        for (int q = lo; q < hi; ++q) (q < mid ? n_big : n_small) += host_bins[q];
+        if (!may_sync || n_big) rc = launch_one(c, lo, mid, n_big, max_m, c);
+        if (rc == 0 && (!may_sync || n_small))
+          rc = launch_one(c, mid, hi, n_small, std::min<int64_t>(max_m, tier_m), c + 1);
+        continue;
+      }
+      rc = launch_one(c, lo, hi, host_counts[c], max_m, c);
     }
   }
   CUDA_TRY(cudaFreeAsync(ws, s));
