@@ -211,12 +211,19 @@ __device__ __forceinline__ uint32_t ldg_u16_if(const void* addr, bool pred) {
       : "memory");
   return v;
 }
-__device__ __forceinline__ uint32_t atomic_add_if(uint32_t* addr, bool pred) {
+// Ticket claim by the predicated lane. The address carries a lane-dependent
+// zero (lane * zero, zero = a run-time 0 such as KParams::pk.zero) so ptxas
+// cannot prove it warp-uniform: a uniform-address atomic is rewritten into the
+// warp-aggregated form (VOTEU/POPC/leader ATOMG + an immediate SHFL of the
+// result), which stalls on the atomic's round trip right here instead of where
+// the ticket is consumed, one LP later.
+__device__ __forceinline__ uint32_t atomic_add_if(uint32_t* addr, bool pred, uint64_t zero) {
   uint32_t v = 0;
+  const uint32_t* a = addr + (uint64_t)(threadIdx.x & 31) * zero;
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q atom.global.add.u32 %0, [%1], 1;\n\t}"
       : "+r"(v)
-      : "l"(addr), "r"((uint32_t)pred)
+      : "l"(a), "r"((uint32_t)pred)
       : "memory");
   return v;
 }
@@ -672,7 +679,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
   int64_t g = (int64_t)blockIdx.x * kLaneWarps + wic;
   while (g < groups) {
     // next group's ticket now; consumed after this group (one group ahead)
-    const uint32_t ticket = atomic_add_if(p.counter, lane == 0);
+    const uint32_t ticket = atomic_add_if(p.counter, lane == 0, p.pk.zero);
     const int64_t j = g * 32 + lane;
     Header<T> h;
     h.lp = j < n_list ? (list ? (int64_t)list[j] : j) : -1;
@@ -937,7 +944,7 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
     policy = policy_evict_first();
     lpN = lp_of(blockIdx.x);
     hwN = load_header_word<T>(p, lpN, lane);
-    ticket = atomic_add_if(p.counter, lane == 0);
+    ticket = atomic_add_if(p.counter, lane == 0, p.pk.zero);
     if (lane == 0) mbar_init(&sh.bar, 1);
   }
   uint32_t phase = 0;
@@ -963,7 +970,7 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
       }
       lpN = lp_of((int64_t)__shfl_sync(kFull, ticket, 0) + G);
       hwN = load_header_word<T>(p, lpN, lane);
-      ticket = atomic_add_if(p.counter, lane == 0);
+      ticket = atomic_add_if(p.counter, lane == 0, p.pk.zero);
     }
     __syncthreads();  // header visible (and the previous LP's reads are done)
     const Header<T> h = sh.hdr;
