@@ -111,7 +111,8 @@ struct WarpLayout {
   static constexpr int blocks_for(int w) { return (int)((227u * 1024u) / (w * kBuf + w * 8u)); }
   static constexpr int best_warps() {
     int bw = 4;
-    for (int w = 5; w <= (NT > 0 ? 7 : 5); ++w)
+    // (fp64: 4, so 3 CTAs/SM leave 170 registers per thread)
+    for (int w = 5; w <= (NT > 0 ? 7 : (sizeof(T) == 8 ? 4 : 5)); ++w)
       if (blocks_for(w) * w > blocks_for(bw) * bw) bw = w;
     return bw;
   }
@@ -131,7 +132,7 @@ struct WarpLayout {
   // no bound check.
   static constexpr int kAlwaysValid =
       NT > 0 ? NS
-             : (NS == 2 ? 1 : NS == 4 ? 2 : NS == 6 ? 4 : NS == 10 ? 6 : NS == 18 ? 10 : 0);
+             : (NS == 2 ? 1 : NS == 4 ? 2 : NS == 6 ? 4 : NS == 9 ? 6 : NS == 10 ? 9 : NS == 18 ? 10 : 0);
 };
 
 // Per-LP header held by lane 0 between claim and solve.
@@ -1209,7 +1210,7 @@ __device__ __forceinline__ int size_class(int32_t m, const int32_t* slots, int n
 constexpr int kMaxBins = 128;
 
 struct BinSpec {
-  int32_t slots[8];
+  int32_t slots[10];
   int32_t nreg;
   int32_t lane_bins;  // > 0: class 0 is split into one bin per m in [0, lane_bins)
   int32_t cta_bins;   // > 1: the large class is split by m, largest first
