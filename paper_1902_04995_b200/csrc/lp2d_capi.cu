@@ -107,7 +107,7 @@ uint32_t* take_counter(int dev) {
 }
 
 // Register slot classes: NS slots hold m + 4 positions (box included).
-constexpr int kSlotClasses[] = {1, 2, 4, 6, 9, 10, 18, 33, 65};
+constexpr int kSlotClasses[] = {1, 2, 4, 5, 6, 9, 10, 18, 33, 65};
 
 template <typename T>
 constexpr int max_nslot() {
@@ -275,6 +275,7 @@ int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t ma
       return launch_warp_kernel<T, P, 1>(kp, dev, s);
     case 2: return launch_warp_kernel<T, P, 2>(kp, dev, s);
     case 4: return launch_warp_kernel<T, P, 4>(kp, dev, s);
+    case 5: return launch_warp_kernel<T, P, 5>(kp, dev, s);
     case 6: return launch_warp_kernel<T, P, 6>(kp, dev, s);
     case 9: return launch_warp_kernel<T, P, 9>(kp, dev, s);
     case 10: return launch_warp_kernel<T, P, 10>(kp, dev, s);

@@ -132,7 +132,7 @@ struct WarpLayout {
   // no bound check.
   static constexpr int kAlwaysValid =
       NT > 0 ? NS
-             : (NS == 2 ? 1 : NS == 4 ? 2 : NS == 6 ? 4 : NS == 9 ? 6 : NS == 10 ? 9 : NS == 18 ? 10 : 0);
+             : (NS == 2 ? 1 : NS == 4 ? 2 : NS == 5 ? 4 : NS == 6 ? 5 : NS == 9 ? 6 : NS == 10 ? 9 : NS == 18 ? 10 : 0);
 };
 
 // Per-LP header held by lane 0 between claim and solve.
