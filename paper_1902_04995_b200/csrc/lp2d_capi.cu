@@ -332,9 +332,9 @@ int launch_balanced(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStrea
   int32_t* cursors = counts + kMaxBins;
   int32_t* list = counts + 2 * kMaxBins;
   CUDA_TRY(cudaMemsetAsync(counts, 0, 2 * kMaxBins * sizeof(int32_t), s));
-  const int threads = 256;
-  const int grid = (int)std::min<int64_t>((kp.n_list + threads - 1) / threads,
-                                          (int64_t)g_dev[dev].sm_count * 8);
+  const int threads = 512;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((kp.n_list + threads - 1) / threads,
+                                                               (int64_t)g_dev[dev].sm_count * 2));
   k_bin_count<<<grid, threads, 0, s>>>(kp.n_list, kp.m, spec, counts);
   note_launch();
   k_bin_scatter<<<grid, threads, 0, s>>>(kp.n_list, kp.m, spec, counts, cursors, list);

@@ -1259,43 +1259,77 @@ __device__ __forceinline__ int bin_of(int32_t m, const BinSpec& spec) {
   return base + spec.cta_bins - 1 - q;
 }
 
+// Bin histogram: warp-aggregated shared-memory counts (one shared atomic
+// per (warp, bin)), then one global atomic per (block, non-empty bin). The
+// grid is a small multiple of the SM count, so the hot bins of a skewed size
+// distribution see a few hundred global atomics, not one per warp.
 __global__ void k_bin_count(int64_t n, const int32_t* m, BinSpec spec, int32_t* counts) {
   __shared__ int32_t local[kMaxBins];
   for (int i = threadIdx.x; i < kMaxBins; i += blockDim.x) local[i] = 0;
-  __syncthreads();
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&local[bin_of(m[j], spec)], 1);
-  __syncthreads();
-  for (int i = threadIdx.x; i < kMaxBins; i += blockDim.x)
-    if (local[i]) atomicAdd(&counts[i], local[i]);
-}
-
-__global__ void k_bin_scatter(int64_t n, const int32_t* m, BinSpec spec, const int32_t* counts,
-                              int32_t* cursors, int32_t* list) {
-  // Bin bases once per block; then warp-aggregated slot reservation: one
-  // atomic per (warp, bin) instead of one per LP on the same address.
-  __shared__ int32_t base[kMaxBins];
-  if (threadIdx.x == 0) {
-    int32_t acc = 0;
-    for (int q = 0; q < kMaxBins; ++q) {
-      base[q] = acc;
-      acc += counts[q];
-    }
-  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < n; j0 += stride) {
     const int64_t j = j0 + threadIdx.x;
-    const bool in = j < n;
-    const int c = in ? bin_of(m[j], spec) : kMaxBins - 1;
+    const int c = j < n ? bin_of(m[j], spec) : -1;
+    const uint32_t peers = __match_any_sync(kFull, c);
+    if (c >= 0 && lane == __ffs(peers) - 1) atomicAdd(&local[c], __popc(peers));
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxBins; i += blockDim.x)
+    if (local[i]) atomicAdd(&counts[i], local[i]);
+}
+
+// Scatter of LP indices into per-bin lists. Each block owns one contiguous
+// chunk of LPs: it counts its chunk per bin (warp-aggregated shared atomics),
+// reserves one range per non-empty bin with a single global atomic, then
+// hands out slots inside its ranges with shared atomics. Order inside a bin
+// is unspecified (scheduling only; results are per LP).
+__global__ void k_bin_scatter(int64_t n, const int32_t* m, BinSpec spec, const int32_t* counts,
+                              int32_t* cursors, int32_t* list) {
+  __shared__ int32_t base[kMaxBins];  // global bin start + this block's range
+  __shared__ int32_t cnt[kMaxBins];
+  const int lane = threadIdx.x & 31;
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * chunk, hi = min(n, lo + chunk);
+  for (int i = threadIdx.x; i < kMaxBins; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  for (int64_t j0 = lo; j0 < hi; j0 += blockDim.x) {
+    const int64_t j = j0 + threadIdx.x;
+    const int c = j < hi ? bin_of(m[j], spec) : -1;
+    const uint32_t peers = __match_any_sync(kFull, c);
+    if (c >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[c], __popc(peers));
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive prefix of the global counts, one warp
+    int32_t carry = 0;
+    for (int q0 = 0; q0 < kMaxBins; q0 += 32) {
+      const int32_t v = counts[q0 + lane];
+      int32_t x = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int32_t y = __shfl_up_sync(kFull, x, d);
+        if (lane >= d) x += y;
+      }
+      base[q0 + lane] = carry + x - v;
+      carry += __shfl_sync(kFull, x, 31);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxBins; i += blockDim.x) {
+    if (cnt[i]) base[i] += atomicAdd(&cursors[i], cnt[i]);
+    cnt[i] = 0;
+  }
+  __syncthreads();
+  for (int64_t j0 = lo; j0 < hi; j0 += blockDim.x) {
+    const int64_t j = j0 + threadIdx.x;
+    const int c = j < hi ? bin_of(m[j], spec) : -1;
     const uint32_t peers = __match_any_sync(kFull, c);
     const int leader = __ffs(peers) - 1;
     int32_t slot = 0;
-    if (lane == leader && in) slot = atomicAdd(&cursors[c], __popc(peers));
+    if (c >= 0 && lane == leader) slot = atomicAdd(&cnt[c], __popc(peers));
     slot = __shfl_sync(kFull, slot, leader) + __popc(peers & ((1u << lane) - 1u));
-    if (in) list[base[c] + slot] = (int32_t)j;
+    if (c >= 0) list[base[c] + slot] = (int32_t)j;
   }
 }
 
