@@ -322,7 +322,8 @@ def test_adversarial_inputs_every_warp_class(P, O, dt):
     zero normals (NaN lines), NaN and infinite entries. Bit-identical to the
     oracle in both precisions."""
     rng = np.random.default_rng(21)
-    sizes = np.repeat(np.array([40, 100, 150, 300, 500, 700, 1000, 1500, 2076], np.int32), 6)
+    sizes = np.repeat(np.array([40, 100, 150, 180, 250, 300, 500, 700, 1000, 1500, 2076],
+                               np.int32), 6)
     pb = P.PackedBatch.generate(sizes, 77).astype(dt)
     ax, ay, b = pb.ax, pb.ay, pb.b
     for j in range(pb.n):
