@@ -280,8 +280,8 @@ int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t ma
     case 9: return launch_warp_kernel<T, P, 9>(kp, dev, s);
     case 10: return launch_warp_kernel<T, P, 10>(kp, dev, s);
     case 18: return launch_warp_kernel<T, P, 18>(kp, dev, s);
-    case 33:  // 16 register chunks + 17 shared-memory tail chunks
-      if constexpr (max_nslot<T>() >= 33) return launch_warp_kernel<T, P, 16, 17>(kp, dev, s);
+    case 33:  // 14 register chunks + 19 shared-memory tail chunks
+      if constexpr (max_nslot<T>() >= 33) return launch_warp_kernel<T, P, 14, 19>(kp, dev, s);
       break;
     case 65:  // 16 register chunks + 49 tail chunks (m <= 2076, 29 KB per warp)
       if constexpr (max_nslot<T>() >= 65) return launch_warp_kernel<T, P, 16, 49>(kp, dev, s);
