@@ -64,6 +64,9 @@ struct KParams {
   double eps_par, eps_feas, eps_hi;   // tolerance rounded to the scalar type
   float eps_par_f, eps_feas_f, eps_hi_f;  // (float copies: constant-bank operands)
   int32_t total_warps;
+  // late-TMA warp classes: staging arrays sized to this launch's largest LP
+  // (elements per array, a multiple of 8; 0 = the class capacity)
+  int32_t stage_cap;
   PairConsts pk;  // packed-fp32 constants (lp2d_pair.cuh)
 };
 
@@ -126,6 +129,13 @@ struct WarpLayout {
   static constexpr int kMinB = sizeof(T) == 8 ? LP2D_MIN_BLOCKS_F64 : LP2D_MIN_BLOCKS;
   static constexpr int kMinBlocks =
       blocks_for(kWarps) < 1 ? 1 : (blocks_for(kWarps) < kMinB ? blocks_for(kWarps) : kMinB);
+  // Late-TMA classes are launched with a run-time CTA shape (staging sized to
+  // the launch's largest LP, KParams::stage_cap): launch bounds of the widest
+  // shape, with the register budget of the capacity layout.
+  static constexpr int kMaxWarpsRt = kLateTma ? 8 : kWarps;
+  static constexpr int kMinBlocksRt =
+      kLateTma ? ((kWarps * kMinBlocks + 7) / 8 < 1 ? 1 : (kWarps * kMinBlocks + 7) / 8)
+               : kMinBlocks;
   static constexpr uint32_t kSmem = kWarps * kBuf + kWarps * 8;
   // Register chunks below this index are never past the end of an LP of this
   // size class (m + 4 > 32 * previous class's chunks), so their test needs
@@ -284,15 +294,16 @@ __device__ __forceinline__ Header<T> unpack_header(uint32_t w, int64_t lp) {
 // 1D bulk copies completing on the warp's mbarrier (no bytes if !ok).
 template <typename L, typename T, typename P>
 __device__ __forceinline__ void issue_tma(const KParams& p, const Header<T>& h,
-                                          unsigned char* buf, uint64_t* bar, uint64_t policy) {
+                                          unsigned char* buf, uint64_t* bar, uint64_t policy,
+                                          uint32_t arr = L::kArr) {
   const uint32_t bt = h.ok ? round16((uint32_t)h.m * sizeof(T)) : 0u;
   const uint32_t bp = h.ok ? round16((uint32_t)h.m * sizeof(P)) : 0u;
   mbar_arrive_expect_tx(bar, 3 * bt + bp);
   if (bt) {
     bulk_g2s(buf, static_cast<const T*>(p.ax) + h.off, bt, bar, policy);
-    bulk_g2s(buf + L::kArr, static_cast<const T*>(p.ay) + h.off, bt, bar, policy);
-    bulk_g2s(buf + 2 * L::kArr, static_cast<const T*>(p.b) + h.off, bt, bar, policy);
-    bulk_g2s(buf + 3 * L::kArr, static_cast<const P*>(p.perm) + h.off, bp, bar, policy);
+    bulk_g2s(buf + arr, static_cast<const T*>(p.ay) + h.off, bt, bar, policy);
+    bulk_g2s(buf + 2 * arr, static_cast<const T*>(p.b) + h.off, bt, bar, policy);
+    bulk_g2s(buf + 3 * arr, static_cast<const P*>(p.perm) + h.off, bp, bar, policy);
   }
 }
 
