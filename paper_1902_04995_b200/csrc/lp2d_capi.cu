@@ -123,55 +123,51 @@ double eps_hi_of(double eps_par) {
   return (double)hi;
 }
 
-// Late-TMA classes: the staging buffers are sized to the launch's largest LP
-// (max_m, rounded up to 8 elements) and the CTA shape (4..8 warps) is the one
-// with the most resident warps under the shared-memory and register limits:
-// m = 1024 (config 2) fits 16 warps per SM instead of the capacity layout's 15.
-template <typename T, typename P, int NS, int NT>
-int launch_late_tma(KParams kp, int64_t max_m, int dev, cudaStream_t stream) {
-  using L = WarpLayout<T, P, NS, NT>;
-  auto kern = k_solve_warp<T, P, NS, NT>;
-  int64_t cap = max_m > 0 ? std::min<int64_t>(max_m, L::kCap) : L::kCap;
-  cap = std::min<int64_t>((cap + 7) & ~int64_t(7), L::kCap);
-  const size_t arr = ((size_t)cap * sizeof(T) + 15) & ~size_t(15);
-  const size_t bufb = 3 * arr + (((size_t)cap * sizeof(P) + 15) & ~size_t(15));
+// Late-TMA classes: the CTA shape (4..8 warps) with the most resident warps
+// under the shared-memory and register limits is picked at launch, and a
+// launch whose LPs all have m <= 1024 uses the CAP = 1024 layout of the
+// config-2 class (14.4 KB per warp: 16 warps/SM instead of 15).
+template <typename T, typename P, int NS, int NT, int CAP>
+int launch_late_tma_cap(KParams kp, int dev, cudaStream_t stream) {
+  using L = WarpLayout<T, P, NS, NT, CAP>;
+  auto kern = k_solve_warp<T, P, NS, NT, CAP>;
   struct Shape {
     int warps = 0, blocks = 0;
   };
-  static Shape shape[64][2];  // per device: [0] capacity layout, [1] m <= 1024 ... keyed below
-  static int64_t shape_cap[64][2] = {{0}};
-  static bool attr_set[64] = {false};
-  if (!attr_set[dev]) {
+  static Shape shape[64];
+  if (!shape[dev].warps) {
     int optin = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    attr_set[dev] = true;
-  }
-  const int slot = cap == L::kCap ? 0 : 1;
-  if (shape_cap[dev][slot] != cap) {
     Shape best;
     for (int w = 4; w <= L::kMaxWarpsRt; ++w) {
       int b = 0;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, w * 32,
-                                                             w * (bufb + 8)));
+                                                             (size_t)w * (L::kBuf + 8)));
       if (b * w > best.blocks * best.warps) best = Shape{w, b};
     }
     if (best.blocks < 1) return fail(LP2D_ERR_CUDA, "warp kernel does not fit on an SM");
-    shape[dev][slot] = best;
-    shape_cap[dev][slot] = cap;
+    shape[dev] = best;
   }
-  const Shape sh = shape[dev][slot];
-  const size_t smem = (size_t)sh.warps * (bufb + 8);
+  const Shape sh = shape[dev];
+  const size_t smem = (size_t)sh.warps * (L::kBuf + 8);
   const int64_t want = (kp.n_list + sh.warps - 1) / sh.warps;
   const int64_t maxb = (int64_t)sh.blocks * g_dev[dev].sm_count;
   const int grid = (int)std::max<int64_t>(1, std::min(want, maxb));
   kp.total_warps = grid * sh.warps;
-  kp.stage_cap = (int32_t)cap;
   kp.counter = take_counter(dev);
   kern<<<grid, sh.warps * 32, smem, stream>>>(kp);
   note_launch();
   CUDA_TRY(cudaGetLastError());
   return 0;
+}
+
+template <typename T, typename P, int NS, int NT>
+int launch_late_tma(KParams kp, int64_t max_m, int dev, cudaStream_t stream) {
+  if constexpr (NS + NT == 33) {
+    if (max_m > 0 && max_m <= 1024) return launch_late_tma_cap<T, P, NS, NT, 1024>(kp, dev, stream);
+  }
+  return launch_late_tma_cap<T, P, NS, NT, 0>(kp, dev, stream);
 }
 
 template <typename T, typename P, int NS, int NT = 0>

@@ -64,9 +64,6 @@ struct KParams {
   double eps_par, eps_feas, eps_hi;   // tolerance rounded to the scalar type
   float eps_par_f, eps_feas_f, eps_hi_f;  // (float copies: constant-bank operands)
   int32_t total_warps;
-  // late-TMA warp classes: staging arrays sized to this launch's largest LP
-  // (elements per array, a multiple of 8; 0 = the class capacity)
-  int32_t stage_cap;
   PairConsts pk;  // packed-fp32 constants (lp2d_pair.cuh)
 };
 
@@ -95,12 +92,16 @@ __host__ __device__ constexpr uint32_t round16(uint32_t x) {
 // in insertion order and are walked by rolled loops, which keeps the hot code
 // under the SM's instruction cache. The staging buffer receives one LP of up
 // to kCap constraints (original order + permutation) by 1D bulk TMA.
-template <typename T, typename P, int NS, int NT>
+// CAP (late-TMA classes): a smaller data capacity for launches whose LPs all
+// have m <= CAP (config 2: m = 1024 → 14.4 KB per warp, 16 warps/SM); the
+// permutation array keeps the class capacity so every chunk index stays in it.
+template <typename T, typename P, int NS, int NT, int CAP = 0>
 struct WarpLayout {
   static constexpr int kChunks = NS + NT;
-  static constexpr int kCap = 32 * kChunks - 4;
+  static constexpr int kCap = CAP ? CAP : 32 * kChunks - 4;
+  static constexpr int kPermCap = 32 * kChunks - 4;
   static constexpr uint32_t kArr = round16(kCap * sizeof(T));
-  static constexpr uint32_t kPerm = round16(kCap * sizeof(P));
+  static constexpr uint32_t kPerm = round16(kPermCap * sizeof(P));
   static constexpr uint32_t kStage = 3 * kArr + kPerm;
   // The tail is read in place from the staging buffer (through the
   // permutation), so the buffer lives until the LP is solved and the next
@@ -129,9 +130,9 @@ struct WarpLayout {
   static constexpr int kMinB = sizeof(T) == 8 ? LP2D_MIN_BLOCKS_F64 : LP2D_MIN_BLOCKS;
   static constexpr int kMinBlocks =
       blocks_for(kWarps) < 1 ? 1 : (blocks_for(kWarps) < kMinB ? blocks_for(kWarps) : kMinB);
-  // Late-TMA classes are launched with a run-time CTA shape (staging sized to
-  // the launch's largest LP, KParams::stage_cap): launch bounds of the widest
-  // shape, with the register budget of the capacity layout.
+  // Late-TMA classes are launched with a run-time CTA shape (4..8 warps, the
+  // most resident warps for this layout): launch bounds of the widest shape,
+  // with the register budget of the best compile-time shape.
   static constexpr int kMaxWarpsRt = kLateTma ? 8 : kWarps;
   static constexpr int kMinBlocksRt =
       kLateTma ? ((kWarps * kMinBlocks + 7) / 8 < 1 ? 1 : (kWarps * kMinBlocks + 7) / 8)
