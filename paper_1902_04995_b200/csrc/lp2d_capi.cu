@@ -327,7 +327,7 @@ int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t ma
     case 6: return launch_warp_kernel<T, P, 6>(kp, dev, s);
     case 9:
       // fp64: 4 register chunks + 5 shared-memory tail chunks (late TMA)
-      if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 4, 5>(kp, dev, s, max_m);
+      if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 7>(kp, dev, s, max_m);
       return launch_warp_kernel<T, P, 9>(kp, dev, s);
     case 10: return launch_warp_kernel<T, P, 10>(kp, dev, s);
     case 18: return launch_warp_kernel<T, P, 18>(kp, dev, s);
