@@ -324,13 +324,19 @@ int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t ma
     case 2: return launch_warp_kernel<T, P, 2>(kp, dev, s);
     case 4: return launch_warp_kernel<T, P, 4>(kp, dev, s);
     case 5: return launch_warp_kernel<T, P, 5>(kp, dev, s);
-    case 6: return launch_warp_kernel<T, P, 6>(kp, dev, s);
+    case 6:
+      if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 4>(kp, dev, s, max_m);
+      return launch_warp_kernel<T, P, 6>(kp, dev, s);
     case 9:
       // fp64: 4 register chunks + 5 shared-memory tail chunks (late TMA)
       if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 7>(kp, dev, s, max_m);
       return launch_warp_kernel<T, P, 9>(kp, dev, s);
-    case 10: return launch_warp_kernel<T, P, 10>(kp, dev, s);
-    case 18: return launch_warp_kernel<T, P, 18>(kp, dev, s);
+    case 10:
+      if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 8>(kp, dev, s, max_m);
+      return launch_warp_kernel<T, P, 10>(kp, dev, s);
+    case 18:
+      if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 16>(kp, dev, s, max_m);
+      return launch_warp_kernel<T, P, 8, 10>(kp, dev, s, max_m);
     case 33:  // 14 register chunks + 19 shared-memory tail chunks
       if constexpr (max_nslot<T>() >= 33) return launch_warp_kernel<T, P, 14, 19>(kp, dev, s, max_m);
       break;

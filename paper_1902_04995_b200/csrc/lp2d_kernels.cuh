@@ -135,7 +135,8 @@ struct WarpLayout {
   // with the register budget of the best compile-time shape.
   static constexpr int kMaxWarpsRt = kLateTma ? 8 : kWarps;
   static constexpr int kMinBlocksRt =
-      kLateTma ? ((kWarps * kMinBlocks + 7) / 8 < 1 ? 1 : (kWarps * kMinBlocks + 7) / 8)
+      kLateTma ? ((kWarps * kMinBlocks + 7) / 8 < 1 ? 1
+                  : ((kWarps * kMinBlocks + 7) / 8 > 2 ? 2 : (kWarps * kMinBlocks + 7) / 8))
                : kMinBlocks;
   static constexpr uint32_t kSmem = kWarps * kBuf + kWarps * 8;
   // Register chunks below this index are never past the end of an LP of this
