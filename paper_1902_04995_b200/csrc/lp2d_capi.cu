@@ -343,7 +343,7 @@ int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t ma
       return launch_warp_kernel<T, P, 10>(kp, dev, s);
     case 18:
       if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 16>(kp, dev, s, max_m);
-      return launch_warp_kernel<T, P, 8, 10>(kp, dev, s, max_m);
+      return launch_warp_kernel<T, P, 10, 8>(kp, dev, s, max_m);
     case 33:  // 14 register chunks + 19 shared-memory tail chunks
       if constexpr (max_nslot<T>() >= 33) return launch_warp_kernel<T, P, 14, 19>(kp, dev, s, max_m);
       break;
