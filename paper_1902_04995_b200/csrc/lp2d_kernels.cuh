@@ -713,35 +713,42 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
     const int mmax = __reduce_max_sync(kFull, (uint32_t)mj);
     uint32_t pmax = 0;
     decltype(float_bits(T(0))) sbits = float_bits(T(1));
-    // The LP's whole permutation in a few independent 16-byte loads (segments
-    // start 8-element aligned and are padded to 8 elements: the layout
-    // contract), then the data gathered 8 positions (24 independent loads)
-    // per round trip instead of one dependent perm -> data pair per position.
+    // The permutation by 16-byte loads (segments start 8-element aligned and
+    // are padded to 8 elements: the layout contract), one batch of 8
+    // positions ahead of the data, which is gathered 8 positions (24
+    // independent loads) per round trip instead of one dependent perm -> data
+    // pair per position.
     constexpr int PV = 16 / (int)sizeof(P);  // permutation entries per vector
-    constexpr int NPV = (MAXM + PV - 1) / PV;
-    uint32_t o[NPV * PV];
+    constexpr int GB = 8;                    // positions per gather batch
+    constexpr int VB = GB / PV;              // vectors per batch
+    uint4 wv[VB];
 #pragma unroll
-    for (int v = 0; v < NPV; ++v) {
-      uint4 w = make_uint4(0u, 0u, 0u, 0u);
-      if (v * PV < mj) w = __ldg(reinterpret_cast<const uint4*>(gp) + v);
-      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+    for (int v = 0; v < VB; ++v)
+      wv[v] = v * PV < mj ? __ldg(reinterpret_cast<const uint4*>(gp) + v) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int e = 0; e < PV; ++e) {
-        const uint32_t q = sizeof(P) == 2 ? ((ww[e / 2] >> (16 * (e & 1))) & 0xffffu) : ww[e];
-        o[v * PV + e] = v * PV + e < mj ? q : 0u;
-      }
-    }
-    constexpr int GB = 8;  // positions per gather batch
-#pragma unroll
-    for (int k0 = 0; k0 < NPV * PV && k0 < MAXM; k0 += GB) {
+    for (int k0 = 0; k0 < MAXM; k0 += GB) {
       if (k0 >= mmax) break;
+      uint32_t o[GB];
+#pragma unroll
+      for (int v = 0; v < VB; ++v) {
+        const uint32_t ww[4] = {wv[v].x, wv[v].y, wv[v].z, wv[v].w};
+#pragma unroll
+        for (int e = 0; e < PV; ++e)
+          o[v * PV + e] = sizeof(P) == 2 ? ((ww[e / 2] >> (16 * (e & 1))) & 0xffffu) : ww[e];
+      }
+      // next batch's permutation vectors (off this batch's dependency chain)
+#pragma unroll
+      for (int v = 0; v < VB; ++v) {
+        const int e0 = k0 + GB + v * PV;
+        wv[v] = e0 < mj ? __ldg(reinterpret_cast<const uint4*>(gp + e0)) : make_uint4(0, 0, 0, 0);
+      }
       T vx[GB], vy[GB], vb[GB];
 #pragma unroll
       for (int u = 0; u < GB; ++u) {
         const int k = k0 + u;
         if (k < MAXM && k < mj) {
-          pmax = max(pmax, o[k]);
-          const uint32_t oc = min(o[k], (uint32_t)(mj - 1));
+          pmax = max(pmax, o[u]);
+          const uint32_t oc = min(o[u], (uint32_t)(mj - 1));
           vx[u] = gx[oc];
           vy[u] = gy[oc];
           vb[u] = gb[oc];
