@@ -111,7 +111,7 @@ constexpr int kSlotClasses[] = {1, 2, 4, 5, 6, 9, 10, 18, 33, 65};
 
 template <typename T>
 constexpr int max_nslot() {
-  return sizeof(T) == 4 ? 65 : 18;  // fp64 keeps m <= 572 in registers
+  return 65;  // warp classes up to m <= 2076 (larger LPs: the CTA kernel)
 }
 
 // Eps_par rounded up by 2^-10 (relative), in T: the parallel-filter factor.
@@ -123,7 +123,7 @@ double eps_hi_of(double eps_par) {
   return (double)hi;
 }
 
-// Late-TMA classes: the CTA shape (4..8 warps) with the most resident warps
+// Late-TMA classes: the CTA shape (1..8 warps) with the most resident warps
 // under the shared-memory and register limits is picked at launch, and a
 // launch whose LPs all have m <= 1024 uses the CAP = 1024 layout of the
 // config-2 class (14.4 KB per warp: 16 warps/SM instead of 15).
@@ -140,7 +140,7 @@ int launch_late_tma_cap(KParams kp, int dev, cudaStream_t stream) {
     CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     Shape best;
-    for (int w = 4; w <= L::kMaxWarpsRt; ++w) {
+    for (int w = 1; w <= L::kMaxWarpsRt; ++w) {
       int b = 0;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, w * 32,
                                                              (size_t)w * (L::kBuf + 8)));
@@ -328,28 +328,28 @@ int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t ma
     case 2: return launch_warp_kernel<T, P, 2>(kp, dev, s);
     case 4:
       if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 2>(kp, dev, s, max_m);
-      return launch_warp_kernel<T, P, 4>(kp, dev, s);
+      else return launch_warp_kernel<T, P, 4>(kp, dev, s);
     case 5:
       if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 3>(kp, dev, s, max_m);
-      return launch_warp_kernel<T, P, 5>(kp, dev, s);
+      else return launch_warp_kernel<T, P, 5>(kp, dev, s);
     case 6:
       if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 4>(kp, dev, s, max_m);
-      return launch_warp_kernel<T, P, 6>(kp, dev, s);
+      else return launch_warp_kernel<T, P, 6>(kp, dev, s);
     case 9:
       if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 7>(kp, dev, s, max_m);
-      return launch_warp_kernel<T, P, 9>(kp, dev, s);
+      else return launch_warp_kernel<T, P, 9>(kp, dev, s);
     case 10:
       if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 8>(kp, dev, s, max_m);
-      return launch_warp_kernel<T, P, 10>(kp, dev, s);
+      else return launch_warp_kernel<T, P, 10>(kp, dev, s);
     case 18:
       if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 16>(kp, dev, s, max_m);
-      return launch_warp_kernel<T, P, 10, 8>(kp, dev, s, max_m);
-    case 33:  // 14 register chunks + 19 shared-memory tail chunks
-      if constexpr (max_nslot<T>() >= 33) return launch_warp_kernel<T, P, 14, 19>(kp, dev, s, max_m);
-      break;
-    case 65:  // 16 register chunks + 49 tail chunks (m <= 2076, 29 KB per warp)
-      if constexpr (max_nslot<T>() >= 65) return launch_warp_kernel<T, P, 16, 49>(kp, dev, s, max_m);
-      break;
+      else return launch_warp_kernel<T, P, 10, 8>(kp, dev, s, max_m);
+    case 33:  // 14 register chunks + 19 shared-memory tail chunks (fp64: 2 + 31)
+      if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 31>(kp, dev, s, max_m);
+      else return launch_warp_kernel<T, P, 14, 19>(kp, dev, s, max_m);
+    case 65:  // 16 register chunks + 49 tail chunks (m <= 2076, 29 KB per warp; fp64 2 + 63)
+      if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 63>(kp, dev, s, max_m);
+      else return launch_warp_kernel<T, P, 16, 49>(kp, dev, s, max_m);
   }
   return fail(LP2D_ERR_UNSUPPORTED, "size class not built");
 }

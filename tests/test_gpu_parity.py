@@ -130,7 +130,7 @@ def test_large_lps_both_precisions(P, O):
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
 def test_size_class_edges(P, O, dt):
-    cap = 1052 if dt == np.float32 else 540
+    cap = 1052
     sizes = np.array([0, 1, 2, 3, 4, 27, 28, 29, 31, 32, 60, 61, 92, 93, 156, 157, 284, 285,
                       540, 541 if dt == np.float32 else 539, cap], np.int32)
     pb = P.PackedBatch.generate(np.repeat(sizes, 3), 21).astype(dt)
