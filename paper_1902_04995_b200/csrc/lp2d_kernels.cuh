@@ -309,6 +309,37 @@ __device__ __forceinline__ void issue_tma(const KParams& p, const Header<T>& h,
   }
 }
 
+// issue_tma called by the whole warp: the operands are made warp-uniform by
+// REDUX (results in uniform registers), so lane 0 issues the bulk copies
+// with them directly instead of ptxas's per-lane waterfall loop around each
+// UBLKCP (the header values are equal on every lane already).
+template <typename L, typename T, typename P>
+__device__ __forceinline__ void issue_tma_warp(const KParams& p, const Header<T>& h,
+                                               unsigned char* buf, uint64_t* bar,
+                                               uint64_t policy, uint32_t arr, int lane) {
+  const bool go = h.lp >= 0;
+  const uint32_t m = __reduce_max_sync(kFull, h.ok ? (uint32_t)h.m : 0u);
+  const uint32_t olo = __reduce_max_sync(kFull, (uint32_t)(uint64_t)h.off);
+  const uint32_t ohi = __reduce_max_sync(kFull, (uint32_t)((uint64_t)h.off >> 32));
+  const uint32_t sbuf = __reduce_max_sync(kFull, smem_u32(buf));
+  const uint32_t sbar = __reduce_max_sync(kFull, smem_u32(bar));
+  const uint32_t plo = __reduce_max_sync(kFull, (uint32_t)policy);
+  const uint32_t phi = __reduce_max_sync(kFull, (uint32_t)(policy >> 32));
+  const int64_t off = (int64_t)(((uint64_t)ohi << 32) | olo);
+  const uint64_t pol = ((uint64_t)phi << 32) | plo;
+  const uint32_t bt = round16(m * (uint32_t)sizeof(T));
+  const uint32_t bp = round16(m * (uint32_t)sizeof(P));
+  if (lane == 0 && go) {
+    mbar_arrive_expect_tx_u(sbar, 3 * bt + bp);
+    if (bt) {
+      bulk_g2s_u(sbuf, static_cast<const T*>(p.ax) + off, bt, sbar, pol);
+      bulk_g2s_u(sbuf + arr, static_cast<const T*>(p.ay) + off, bt, sbar, pol);
+      bulk_g2s_u(sbuf + 2 * arr, static_cast<const T*>(p.b) + off, bt, sbar, pol);
+      bulk_g2s_u(sbuf + 3 * arr, static_cast<const P*>(p.perm) + off, bp, sbar, pol);
+    }
+  }
+}
+
 // Defining-pair export: box k -> -(k+1), user position 4+i -> perm[i].
 __device__ __forceinline__ int32_t pair_code(uint32_t pos, uint32_t orig) {
   if (pos == kNone) return (int32_t)0x80000000;
