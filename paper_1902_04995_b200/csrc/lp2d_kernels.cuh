@@ -292,27 +292,12 @@ __device__ __forceinline__ Header<T> unpack_header(uint32_t w, int64_t lp) {
   return h;
 }
 
-// Lane 0: stage an LP's ax/ay/b/perm segments into the warp's buffer with
-// 1D bulk copies completing on the warp's mbarrier (no bytes if !ok).
-template <typename L, typename T, typename P>
-__device__ __forceinline__ void issue_tma(const KParams& p, const Header<T>& h,
-                                          unsigned char* buf, uint64_t* bar, uint64_t policy,
-                                          uint32_t arr = L::kArr) {
-  const uint32_t bt = h.ok ? round16((uint32_t)h.m * sizeof(T)) : 0u;
-  const uint32_t bp = h.ok ? round16((uint32_t)h.m * sizeof(P)) : 0u;
-  mbar_arrive_expect_tx(bar, 3 * bt + bp);
-  if (bt) {
-    bulk_g2s(buf, static_cast<const T*>(p.ax) + h.off, bt, bar, policy);
-    bulk_g2s(buf + arr, static_cast<const T*>(p.ay) + h.off, bt, bar, policy);
-    bulk_g2s(buf + 2 * arr, static_cast<const T*>(p.b) + h.off, bt, bar, policy);
-    bulk_g2s(buf + 3 * arr, static_cast<const P*>(p.perm) + h.off, bp, bar, policy);
-  }
-}
-
-// issue_tma called by the whole warp: the operands are made warp-uniform by
-// REDUX (results in uniform registers), so lane 0 issues the bulk copies
-// with them directly instead of ptxas's per-lane waterfall loop around each
-// UBLKCP (the header values are equal on every lane already).
+// Stage an LP's ax/ay/b/perm segments into the warp's buffer with 1D bulk
+// copies completing on the warp's mbarrier (no bytes if !ok). Called by the
+// whole warp: the operands are made warp-uniform by REDUX (results in uniform
+// registers), so lane 0 issues the bulk copies with them directly instead of
+// ptxas's per-lane waterfall loop around each UBLKCP (the header values are
+// equal on every lane already).
 template <typename L, typename T, typename P>
 __device__ __forceinline__ void issue_tma_warp(const KParams& p, const Header<T>& h,
                                                unsigned char* buf, uint64_t* bar,
