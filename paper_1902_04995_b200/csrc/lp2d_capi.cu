@@ -107,11 +107,11 @@ uint32_t* take_counter(int dev) {
 }
 
 // Register slot classes: NS slots hold m + 4 positions (box included).
-constexpr int kSlotClasses[] = {1, 2, 4, 5, 6, 9, 10, 18, 33, 65};
+constexpr int kSlotClasses[] = {1, 2, 4, 5, 6, 9, 10, 18, 33, 65, 129};
 
 template <typename T>
 constexpr int max_nslot() {
-  return 65;  // warp classes up to m <= 2076 (larger LPs: the CTA kernel)
+  return 129;  // warp classes up to m <= 4124 (larger LPs: the CTA kernel)
 }
 
 // Eps_par rounded up by 2^-10 (relative), in T: the parallel-filter factor.
@@ -350,6 +350,9 @@ int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t ma
     case 65:  // 16 register chunks + 49 tail chunks (m <= 2076, 29 KB per warp; fp64 2 + 63)
       if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 63>(kp, dev, s, max_m);
       else return launch_warp_kernel<T, P, 16, 49>(kp, dev, s, max_m);
+    case 129:
+      if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 127>(kp, dev, s, max_m);
+      else return launch_warp_kernel<T, P, 16, 113>(kp, dev, s, max_m);
   }
   return fail(LP2D_ERR_UNSUPPORTED, "size class not built");
 }

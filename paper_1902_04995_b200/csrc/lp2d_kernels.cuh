@@ -1274,7 +1274,7 @@ __device__ __forceinline__ int size_class(int32_t m, const int32_t* slots, int n
 constexpr int kMaxBins = 128;
 
 struct BinSpec {
-  int32_t slots[10];
+  int32_t slots[12];
   int32_t nreg;
   int32_t lane_bins;  // > 0: class 0 is split into one bin per m in [0, lane_bins)
   int32_t cta_bins;   // > 1: the large class is split by m, largest first
