@@ -84,7 +84,8 @@ def load_traffic(cfg_name):
 
 
 class ClockSampler:
-    """nvidia-smi sampling of SM clocks and throttle reasons during a region."""
+    """SM clocks and throttle reasons sampled during a region: NVML polled every
+    ~0.5 ms from a thread (nvidia-smi -lms 100 as the fallback)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -94,8 +95,40 @@ class ClockSampler:
         self.gpu = gpu_index
         self.samples = []
         self.proc = None
+        self.nvml = None
+        self.stop = False
+
+    def _poll_nvml(self):
+        # NVML polled every ~0.5 ms: a timed region of a few ms still gets
+        # samples taken while the kernels run (nvidia-smi -lms is >= 100 ms)
+        N, h = self.nvml
+        bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+        while not self.stop:
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(sm), str(mx)] +
+                                    ["Active" if r & b else "Not Active" for b in bits])
+            except Exception:
+                return
+            time.sleep(0.0005)
 
     def __enter__(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            self.nvml = (N, N.nvmlDeviceGetHandleByIndex(self.gpu))
+            self.thread = threading.Thread(target=self._poll_nvml, daemon=True)
+            self.thread.start()
+            t0 = time.perf_counter()  # sampling is running before the region starts
+            while not self.samples and time.perf_counter() - t0 < 0.05:
+                time.sleep(0.0002)
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
@@ -114,6 +147,17 @@ class ClockSampler:
                 self.samples.append(parts)
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self.stop = True
+            self.thread.join(timeout=5)
+            if not self.samples:  # (a region shorter than one poll)
+                self.stop = False
+                t = threading.Thread(target=self._poll_nvml, daemon=True)
+                t.start()
+                time.sleep(0.002)
+                self.stop = True
+                t.join(timeout=5)
+            return
         if self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
