@@ -1265,10 +1265,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_solve_global(const __grid
 // (nclass - 1). Two passes: count, then scatter ids into class-contiguous
 // segments of `list` (order within a class is irrelevant: LPs are
 // independent).
+// Branch-free: the class is the number of classes too small for m (slots
+// ascend), counted over a fixed-size unrolled table (no dynamic indexing of
+// the parameter array, no loop-carried branch).
 __device__ __forceinline__ int size_class(int32_t m, const int32_t* slots, int nreg) {
-  for (int c = 0; c < nreg; ++c)
-    if (m + 4 <= 32 * slots[c]) return c;
-  return nreg;
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) c += (k < nreg && m + 4 > 32 * slots[k]) ? 1 : 0;
+  return c;
 }
 
 constexpr int kMaxBins = 128;
