@@ -23,8 +23,14 @@ roofline  : algorithmic bytes 3*sizeof(T)*m per LP over
 cpu_baseline / --impl reference : the unmodified reference (oracle/_ref, the
             reference headers compiled by oracle/Makefile) timed on this
             box's host cores — solve_batch(balanced, width 512, workers = all
-            hardware threads) on the same instances, in fp64 (the reference
-            has no fp32 path; fp32 configs feed it the fp32-rounded inputs).
+            hardware threads) on the same instances. fp32 configs store the
+            instance in float (12 B per constraint); both arms compute the
+            reference's double arithmetic on those values (the reference arm
+            widens them), so both produce the same results. The reference arm
+            builds its inputs with the reference's own generator (oracle/_ref
+            ref_fill), never loading the product library.
+--dtype f64 : store a config's instance in double instead (24 B per
+            constraint; the like-for-like input of the reference's API).
 """
 from __future__ import annotations
 
@@ -178,7 +184,10 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def pareto_sizes(seed, total=1 << 24):
+def pareto_sizes(seed, total=1 << 24, via="ours"):
+    if via == "reference":
+        O = _oracle()
+        return O.ref_pareto_sizes(seed, total)
     import paper_1902_04995_b200 as P
 
     out = np.zeros(total // 8 + 1, np.int32)
@@ -186,36 +195,77 @@ def pareto_sizes(seed, total=1 << 24):
     return out[:k]
 
 
-def make_batch(cfg_name, rank):
-    """SURVEY.md §8(d) workloads; LP j of rank r is global LP r*n + j."""
-    import paper_1902_04995_b200 as P
+def _oracle():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py as O  # baseline infrastructure only (reference arm / cpu_baseline)
 
-    n, m, dt, seed, _ = CONFIGS[cfg_name]
+    return O
+
+
+def config_dtype(cfg_name, dtype_arg):
+    dt = CONFIGS[cfg_name][2]
+    if dtype_arg:
+        dt = np.float32 if dtype_arg == "f32" else np.float64
+    return dt
+
+
+def make_batch(cfg_name, rank, dt, via="ours"):
+    """SURVEY.md §8(d) workloads; LP j of rank r is global LP r*n + j.
+    via="ours": the product's generator (lp2dgen_fill); via="reference": the
+    reference's own generator (oracle/_ref ref_fill), so the reference arm
+    never loads the product library. Both give the same instance bit for bit
+    (tests/test_generate.py)."""
+    n, m, _, seed, _ = CONFIGS[cfg_name]
     kind, bscale = None, 1.0
     if cfg_name == "c4":
-        sizes = pareto_sizes(seed)
+        sizes = pareto_sizes(seed, via=via)
         n = len(sizes)
     else:
         sizes = np.full(n, m, np.int32)
     g = np.arange(rank * n, (rank + 1) * n)
+    FEAS, INF, UNB = 0, 1, 3  # generate.hpp gen_kind (+ the builder's unbounded kind)
     if cfg_name == "c3":
-        kind = np.where(g % 10 == 0, P.GenKind.infeasible, P.GenKind.feasible_random).astype(np.uint8)
+        kind = np.where(g % 10 == 0, INF, FEAS).astype(np.uint8)
         bscale = 2e-7
     elif cfg_name == "c5":
-        kind = np.full(n, int(P.GenKind.feasible_random), np.uint8)
-        kind[g % 10 == 3] = int(P.GenKind.infeasible)
-        kind[g % 10 == 7] = int(P.GenKind.unbounded_random)
-    pb = P.PackedBatch.generate(sizes, seed, first=rank * n, kind=kind, bscale=bscale)
+        kind = np.full(n, FEAS, np.uint8)
+        kind[g % 10 == 3] = INF
+        kind[g % 10 == 7] = UNB
+    if via == "reference":
+        pb = _oracle().ref_fill(sizes, seed, kind=kind, bscale=bscale, first=rank * n)
+        pb.perm = pb.perm.astype(np.uint16) if pb.m.max(initial=0) <= 65536 else pb.perm
+    else:
+        import paper_1902_04995_b200 as P
+
+        pb = P.PackedBatch.generate(sizes, seed, first=rank * n, kind=kind, bscale=bscale)
     return pb.astype(dt) if dt != np.float64 else pb
+
+
+def config_dict(cfg_name, pb, world, dt):
+    """The `config` object of both arms' JSON lines (identical keys/values)."""
+    n, m = pb.n, CONFIGS[cfg_name][1] or float(np.mean(pb.m))
+    return {"workload": CONFIGS[cfg_name][4], "config": cfg_name, "lps_per_gpu": int(n),
+            "m": m, "storage": "f32" if dt == np.float32 else "f64", "arithmetic": "f64",
+            "parallelism": "dp%d (LP-index shards, no collective)" % world}
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def cpu_reference(pb, steps, warmup, threads=0):
     """Time the unmodified reference solve_batch (oracle/_ref) on this host."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle_py as O  # test/baseline infrastructure only
-
+    O = _oracle()
     ref = O.ref_lib()
     n = pb.n
+    # fp32 storage is widened exactly: the reference's doubles on the stored instance
     ax, ay, b = (np.ascontiguousarray(a, np.float64) for a in (pb.ax, pb.ay, pb.b))
     c, M = np.ascontiguousarray(pb.c, np.float64), np.ascontiguousarray(pb.M, np.float64)
     perm = np.ascontiguousarray(pb.perm, np.uint32)
@@ -236,8 +286,10 @@ def cpu_reference(pb, steps, warmup, threads=0):
         ref.ref_batch_free(h)
     total_s = sum(ns) / 1e9
     return {"value": n * steps / total_s, "unit": "LPs/s", "cores": cores, "kind": "reference",
-            "sample": f"{n} LPs x {sizes_desc(pb)} constraints, fp64 solve_batch(balanced, width 512, "
-                      f"{cores} workers) x {steps} runs = {total_s:.2f} s wall"}
+            "cpu_model": cpu_model(),
+            "sample": f"{n} LPs x {sizes_desc(pb)} constraints ({pb.ax.dtype} storage, double "
+                      f"arithmetic), solve_batch(balanced, width 512, {cores} workers) x {steps} "
+                      f"runs = {total_s:.2f} s wall"}
 
 
 def sizes_desc(pb):
@@ -247,23 +299,27 @@ def sizes_desc(pb):
 
 def run_reference_arm(args, world, rank):
     cfg = args.config
-    n, m, dt, seed, desc = CONFIGS[cfg]
     if rank != 0:
         return
-    pb = make_batch(cfg, 0)
-    n, m = pb.n, (m or int(pb.m.mean()))
+    dt = config_dtype(cfg, args.dtype)
+    pb = make_batch(cfg, 0, dt, via="reference")
+    n = pb.n
     cb = cpu_reference(pb, args.steps, args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "LPs/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * n / cb["value"], "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "lps": n, "m": m, "parallelism": "host threads"},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA % CONFIGS[cfg][3],
+        "config": config_dict(cfg, pb, world, dt),
         "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": "LPs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+DATA = ("synthetic: reference generator streams (gen_mixed-style, seed %d), LP j seeded by "
+        "its global index")
 
 
 def main():
@@ -273,6 +329,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default=None, choices=["f32", "f64"],
+                    help="scalar storage (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 5)")
     ap.add_argument("--streams", type=int, default=2,
@@ -306,8 +364,9 @@ def main():
         return float(t.item())
 
     cfg = args.config
-    n, m, dt, seed, desc = CONFIGS[cfg]
-    pb = make_batch(cfg, rank)
+    _, m, _, seed, desc = CONFIGS[cfg]
+    dt = config_dtype(cfg, args.dtype)
+    pb = make_batch(cfg, rank, dt)
     n, m = pb.n, (m or int(pb.m.mean()))
     algo_bytes = pb.constraint_bytes()
 
@@ -396,8 +455,9 @@ def main():
     pin = lambda a: _pinned_copy(torch, a)
     hp = P.PackedBatch(pin(pb.m), pin(pb.offset), pin(pb.ax), pin(pb.ay), pin(pb.b), pin(pb.perm),
                        pin(pb.c), pin(pb.M))
+    f8 = np.float64  # results are the reference's doubles for either storage
     hout = P.PackedResult(*(pin(np.zeros(sh, d)) for sh, d in (
-        (n, np.uint8), (n, dt), (n, dt), (n, dt), ((n, 2), np.int32), (n, np.uint32), (n, np.uint64))))
+        (n, np.uint8), (n, f8), (n, f8), (n, f8), ((n, 2), np.int32), (n, np.uint32), (n, np.uint64))))
     cfgb = P.BlockConfig(workers=1)
     P.solve_packed(hp, cfgb, out=hout)  # warm the library's device arena
     h2d = sum(a.nbytes for a in (hp.m, hp.offset, hp.ax, hp.ay, hp.b, hp.perm, hp.c, hp.M))
@@ -420,12 +480,10 @@ def main():
             "metric": METRIC, "value": value, "unit": "LPs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32" if dt == np.float32 else "f64",
-            "data": "synthetic: reference generator streams (gen_mixed, seed %d), LP j seeded by "
-                    "its global index" % seed,
-            "config": {"workload": desc, "lps_per_gpu": n, "m": m,
-                       "parallelism": "dp%d (LP-index shards, no collective)" % world,
-                       "l2": "inputs %.0f MB > 126 MB L2, no flush" % (h2d / 1e6)},
+            "dtype": "f64", "storage": "f32" if dt == np.float32 else "f64",
+            "data": DATA % seed,
+            "config": config_dict(cfg, pb, world, dt),
+            "l2": "inputs %.0f MB %s 126 MB L2, no flush" % (h2d / 1e6, ">" if h2d > 126e6 else "<"),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": load_traffic(cfg),
                          "peak_source": peak_src,
@@ -439,9 +497,11 @@ def main():
                          "single_stream_value": world * n / (single_ms_per_step / 1e3),
                          "single_stream_gpu_launches": gpu_launches,
                          "achieved_gbps": algo_bytes / (ms_per_step / 1e3) / 1e9,
-                         "note": "value/ms_per_step: K steps alternating over the streams "
-                                 "(independent batches, own result buffers); roofline: "
-                                 "isolated launches of the single-stream loop"},
+                         "note": "value/ms_per_step: K solves of the SAME device-resident "
+                                 "input batch, alternating over the streams with one result "
+                                 "buffer per stream, so one solve's drain overlaps the next "
+                                 "one's ramp-up; roofline: isolated launches of the "
+                                 "single-stream loop"},
             "schedulers": {"balanced_kernel_ms": kern_ms, "naive_kernel_ms": naive_ms,
                            "naive_over_balanced": naive_ms / kern_ms,
                            "note": "naive = thread per LP (paper's RGB naive), balanced = "

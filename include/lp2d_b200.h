@@ -13,8 +13,10 @@
  * Semantics per LP (serial.hpp:159-188): maximise c.x subject to the four box
  * constraints x<=M, -x<=M, y<=M, -y<=M (positions 0..3, never permuted) and the
  * user constraints a.x <= b inserted in the order perm[0..m-1]. Results are
- * bit-identical to the reference's serial solver computing in the same scalar
- * type (fp64: the reference itself; fp32: oracle/ restatement in float).
+ * bit-identical to the reference's serial solver (double arithmetic) on the
+ * stored instance: lp2dgpu_solve_f64 reads double inputs, lp2dgpu_solve_f32
+ * reads float inputs (12 B per constraint in HBM), which are widened exactly,
+ * so both return the reference's own doubles.
  */
 #ifndef LP2D_B200_H
 #define LP2D_B200_H
@@ -101,7 +103,8 @@ typedef struct lp2d_opts {
 } lp2d_opts;
 
 /* Outputs, n entries each (host or device per batch->mem). Optional members
- * may be NULL. x/y/value are float for f32 and double for f64. */
+ * may be NULL. x/y/value are double for both entry points (the reference's
+ * solution::point / value type, serial.hpp:34-43). */
 typedef struct lp2d_out {
   uint8_t* status;
   void* x;

@@ -155,29 +155,25 @@ int lp2d_oracle_gen(int64_t m, uint64_t seed, int kind, double margin,
   return -1;
 }
 
-/* ---- serial.hpp solve, instantiated for double and float ----------------- */
+/* ---- serial.hpp solve: double arithmetic over double or float storage ---- */
 #define T double
+#define S double
 #define SUF d
 #define SQRT sqrt
 #define FABS fabs
 #define FMAX fmax
 #define FMIN fmin
 #include "oracle_solve_impl.h"
-#undef T
+#undef S
 #undef SUF
-#undef SQRT
-#undef FABS
-#undef FMAX
-#undef FMIN
 
-#define T float
+/* fp32 configs: the instance is stored in float; the solve is the
+ * reference's double arithmetic on the exactly widened values. */
+#define S float
 #define SUF f
-#define SQRT sqrtf
-#define FABS fabsf
-#define FMAX fmaxf
-#define FMIN fminf
 #include "oracle_solve_impl.h"
 #undef T
+#undef S
 #undef SUF
 #undef SQRT
 #undef FABS

@@ -6,12 +6,17 @@
  * in __graft_entry__.py and bench.py's cpu_baseline / --impl reference leg may
  * load it. The product (paper_1902_04995_b200/) never links or calls it.
  *
- * Parity pinning: the double instantiation is checked bit-for-bit against the
- * unmodified reference compiled from /root/reference (oracle/_ref, see
- * oracle/Makefile) and against the reference's own golden values
- * (tests/golden/, tests/test_oracle.py). The float instantiation and the
- * status/defining-pair extension have no reference counterpart; they follow
- * the same operation order and are pinned by the committed fixtures only.
+ * Parity pinning: the solver is checked bit-for-bit against the unmodified
+ * reference compiled from /root/reference (oracle/_ref, see oracle/Makefile)
+ * and against the reference's own golden values (tests/golden/,
+ * tests/test_oracle.py). Both entry points compute in double exactly like the
+ * reference: *_d reads double inputs, *_f reads float inputs (the fp32
+ * configs' storage) and widens them exactly, so *_f IS the reference applied
+ * to the fp32-rounded instance (pinned against oracle/_ref on such instances
+ * too). The status/defining-pair extension has no reference counterpart; it
+ * follows the same operation order, is cross-checked against the reference's
+ * brute-force vertex oracle (oracle.hpp:38-70) for m <= 512, and is pinned by
+ * the committed fixtures.
  */
 #ifndef LP2D_ORACLE_H
 #define LP2D_ORACLE_H

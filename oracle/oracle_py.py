@@ -117,6 +117,12 @@ def ref_lib():
         lib.ref_uniform.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_int64, C.c_void_p]
         lib.ref_contention_ns.restype = C.c_int64
         lib.ref_contention_ns.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_uint64, C.c_int64]
+        lib.ref_fill.restype = C.c_int
+        lib.ref_fill.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_double, C.c_double] + [C.c_void_p] * 6
+        lib.ref_pareto_sizes.restype = C.c_int64
+        lib.ref_pareto_sizes.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_int32, C.c_int64,
+                                         C.c_int64, C.c_void_p]
         _ref = lib
     return _ref
 
@@ -192,3 +198,69 @@ def uniform(seed, stream, lo, hi, n, ref=False):
     fn = ref_lib().ref_uniform if ref else oracle_lib().lp2d_oracle_uniform
     fn(seed & (2**64 - 1), stream & (2**64 - 1), lo, hi, n, _p(out))
     return out
+
+
+# ---- the reference's own generator / solver over packed batches ------------
+
+class RefPacked:
+    """Packed SoA batch (the product layout) built by the reference's
+    generator (ref_fill), with no dependency on the product library."""
+
+    def __init__(self, m, offset, ax, ay, b, perm, c, M):
+        self.m, self.offset, self.ax, self.ay, self.b = m, offset, ax, ay, b
+        self.perm, self.c, self.M = perm, c, M
+        self.n = len(m)
+
+    def astype(self, dt):
+        return RefPacked(self.m, self.offset, self.ax.astype(dt), self.ay.astype(dt),
+                         self.b.astype(dt), self.perm, self.c.astype(dt), self.M.astype(dt))
+
+
+def pack_offsets(m):
+    cap = (np.asarray(m, np.int64) + 7) // 8 * 8
+    off = np.zeros(len(m) + 1, np.int64)
+    off[1:] = np.cumsum(cap)
+    return off
+
+
+def ref_fill(m, seed, kind=None, margin=1.0, bscale=1.0, first=0):
+    m = np.ascontiguousarray(m, np.int32)
+    n = len(m)
+    off = pack_offsets(m)
+    E = int(off[-1])
+    ax = np.zeros(E); ay = np.zeros(E); b = np.zeros(E)
+    perm = np.zeros(E, np.uint32); c = np.zeros(2 * n); M = np.zeros(n)
+    kd = None if kind is None else np.ascontiguousarray(np.broadcast_to(np.asarray(kind, np.uint8), (n,)))
+    rc = ref_lib().ref_fill(n, first, seed & (2**64 - 1), _p(m), _p(off), _p(kd), margin, bscale,
+                            _p(ax), _p(ay), _p(b), _p(perm), _p(c), _p(M))
+    if rc:
+        raise ValueError("ref_fill failed")
+    return RefPacked(m, off, ax, ay, b, perm, c, M)
+
+
+def ref_pareto_sizes(seed, total, xmin=8.0, alpha=1.0, xmax=8192):
+    out = np.zeros(int(total // xmin) + 1, np.int32)
+    k = ref_lib().ref_pareto_sizes(seed, xmin, alpha, xmax, total, len(out), _p(out))
+    return out[:k]
+
+
+def ref_solve_batch(packed, threads=0, block_width=512, balanced=True):
+    """lp2d::solve_batch (the unmodified reference) over a packed batch; float
+    storage is widened exactly (the fp32 configs' semantics). Returns
+    (feasible u8, x, y, value, stats[5] = total_wu, violation_events, ...)."""
+    ref = ref_lib()
+    f64 = lambda a: np.ascontiguousarray(a, np.float64)
+    ax, ay, b, c, M = (f64(a) for a in (packed.ax, packed.ay, packed.b, packed.c, packed.M))
+    perm = np.ascontiguousarray(packed.perm, np.uint32)
+    off = np.ascontiguousarray(packed.offset, np.int64)
+    mm = np.ascontiguousarray(packed.m, np.int32)
+    n = len(mm)
+    h = ref.ref_batch_create(n, _p(off), _p(mm), _p(ax), _p(ay), _p(b), _p(perm), _p(c), _p(M))
+    fe = np.zeros(n, np.uint8); x = np.zeros(n); y = np.zeros(n); v = np.zeros(n)
+    st = np.zeros(5, np.uint64)
+    try:
+        ref.ref_batch_solve(h, block_width, 1 if balanced else 0, threads, 1e-12, 1e-9, _p(fe), _p(x),
+                            _p(y), _p(v), _p(st), None)
+    finally:
+        ref.ref_batch_free(h)
+    return fe, x, y, v, st

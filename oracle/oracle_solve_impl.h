@@ -1,12 +1,16 @@
 /* ORACLE — test infrastructure only (see oracle/lp2d_oracle.c header).
  *
  * Scalar-generic body of the CPU restatement of the reference's serial
- * Seidel solver. Included twice by lp2d_oracle.c, once with T=double and once
- * with T=float. Every expression follows the reference operation by operation
- * (no FMA contraction: the file is compiled with -ffp-contract=off), so the
- * T=double instantiation is bit-identical to /root/reference/proj/include/lp2d.
+ * Seidel solver. Included twice by lp2d_oracle.c: arithmetic type T=double
+ * always (the reference computes in double), storage type S=double (fp64
+ * configs) or S=float (fp32 configs: the fp32-stored instance, widened
+ * exactly to double on load, so the result is the reference's own result on
+ * the fp32-rounded instance). Every expression follows the reference
+ * operation by operation (no FMA contraction: the file is compiled with
+ * -ffp-contract=off), so it is bit-identical to
+ * /root/reference/proj/include/lp2d.
  *
- * Macros expected: T, SUF, SQRT, FABS, FMAX, FMIN.
+ * Macros expected: T, S, SUF, SQRT, FABS, FMAX, FMIN.
  */
 
 #define CAT2(a, b) a##b
@@ -90,12 +94,13 @@ static inline void FN(box_)(int k, T M, T* ax, T* ay, T* b) {
  * Inputs are one LP in the original constraint order, with the insertion
  * order perm (indices 0..m-1). perm may be NULL for identity order.
  * Returns 0 on success, -1 if perm is not a permutation index set. */
-int FN(lp2d_oracle_solve_)(const T* cax, const T* cay, const T* cb,
-                           const uint32_t* perm, int64_t m, T cx, T cy, T M,
+int FN(lp2d_oracle_solve_)(const S* cax, const S* cay, const S* cb,
+                           const uint32_t* perm, int64_t m, S cx_s, S cy_s, S M_s,
                            double eps_par_d, double eps_feas_d,
                            lp2d_oracle_result* out) {
   const T eps_par = (T)eps_par_d;
   const T eps_feas = (T)eps_feas_d;
+  const T cx = (T)cx_s, cy = (T)cy_s, M = (T)M_s;
   /* serial.hpp:56-58 initial_optimum: zero components tie toward +M. */
   T px = cx < (T)0 ? -M : M;
   T py = cy < (T)0 ? -M : M;
@@ -109,7 +114,7 @@ int FN(lp2d_oracle_solve_)(const T* cax, const T* cay, const T* cb,
   for (int64_t i = 0; i < m; ++i) {
     const int64_t oi = perm ? (int64_t)perm[i] : i;
     if (oi < 0 || oi >= m) return -1;
-    const T hx = cax[oi], hy = cay[oi], hb = cb[oi];
+    const T hx = (T)cax[oi], hy = (T)cay[oi], hb = (T)cb[oi];
     if (FN(satisfied_)(hx, hy, hb, px, py, eps_feas)) continue;
     viol += 1;
     wu += (uint64_t)(4 + i);
@@ -128,7 +133,7 @@ int FN(lp2d_oracle_solve_)(const T* cax, const T* cay, const T* cb,
     }
     for (int64_t k = 0; k < i; ++k) {
       const int64_t ok = perm ? (int64_t)perm[k] : k;
-      FN(classify_apply_)(&acc, cax[ok], cay[ok], cb[ok], &l, eps_par, eps_feas,
+      FN(classify_apply_)(&acc, (T)cax[ok], (T)cay[ok], (T)cb[ok], &l, eps_par, eps_feas,
                           4 + k);
     }
     /* serial.hpp:95-111 resolve_on_line */
@@ -201,9 +206,9 @@ int FN(lp2d_oracle_solve_)(const T* cax, const T* cay, const T* cb,
 
 /* Batch over the packed SoA layout (offsets into ax/ay/b/perm). */
 static int FN(serial_batch_)(int64_t n, const int64_t* offset,
-                                 const int32_t* m, const T* ax, const T* ay,
-                                 const T* b, const uint32_t* perm, const T* c,
-                                 const T* M, double eps_par, double eps_feas,
+                                 const int32_t* m, const S* ax, const S* ay,
+                                 const S* b, const uint32_t* perm, const S* c,
+                                 const S* M, double eps_par, double eps_feas,
                                  lp2d_oracle_result* out) {
   for (int64_t j = 0; j < n; ++j) {
     const int64_t o = offset[j];

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -107,6 +108,92 @@ int ref_gen_mixed(const int64_t* sizes, int64_t nsizes, int64_t count,
   } catch (const std::exception&) {
     return -1;
   }
+}
+
+// The benchmark workloads built from the reference's own
+// generator, independent of the product library: LP j (global index
+// g = first + j) is gen({m[j], derive_seed(seed, 2g), kind[j], margin}) with
+// insertion order shuffle(m[j], derive_seed(seed, 2g+1)) (generate.hpp:
+// 174-189 streams), b and bound_m scaled by bscale. kind 3 is the builder's
+// "unbounded" kind (no reference counterpart): feasible_random's draws with
+// every normal within +-60 degrees of -c, restated here with the reference's
+// xoshiro256pp. Returns 0, or -1 on a thrown exception / bad kind.
+int ref_fill(int64_t n, int64_t first, uint64_t seed, const int32_t* m,
+             const int64_t* offset, const uint8_t* kind, double margin, double bscale,
+             double* ax, double* ay, double* b, uint32_t* perm, double* c,
+             double* bound_m) {
+  try {
+    constexpr double two_pi = 2.0 * 3.141592653589793238462643383279502884;
+    for (int64_t j = 0; j < n; ++j) {
+      const uint64_t g = static_cast<uint64_t>(first + j);
+      const int k = kind ? static_cast<int>(kind[j]) : 0;
+      const int64_t o = offset[j];
+      const uint64_t ps = lp2d::derive_seed(seed, 2 * g);
+      if (k == 3) {
+        lp2d::xoshiro256pp r(ps);
+        const double phi = two_pi * r.unit();
+        c[2 * j] = std::cos(phi);
+        c[2 * j + 1] = std::sin(phi);
+        const double half = 1e7 / 2.0;
+        const double ix = r.in_range(-half, half), iy = r.in_range(-half, half);
+        for (int64_t q = 0; q < m[j]; ++q) {
+          double theta = two_pi * r.unit();
+          theta = phi + 3.141592653589793 + (theta / two_pi * 2.0 - 1.0) * (3.141592653589793 / 3.0);
+          const double a0 = std::cos(theta), a1 = std::sin(theta);
+          const double slack = margin * (1.0 + 9.0 * r.unit());
+          ax[o + q] = a0;
+          ay[o + q] = a1;
+          b[o + q] = (a0 * ix + a1 * iy) + slack;
+        }
+        bound_m[j] = 1e7;
+      } else if (k == 0 || k == 1 || k == 2) {
+        lp2d::gen_spec spec{static_cast<std::size_t>(m[j]), ps, static_cast<lp2d::gen_kind>(k),
+                            margin};
+        const lp2d::problem p = lp2d::gen(spec);
+        for (std::size_t q = 0; q < p.constraints.size(); ++q) {
+          ax[o + q] = p.constraints[q].a.x;
+          ay[o + q] = p.constraints[q].a.y;
+          b[o + q] = p.constraints[q].b;
+        }
+        c[2 * j] = p.obj.c.x;
+        c[2 * j + 1] = p.obj.c.y;
+        bound_m[j] = p.bound_m;
+      } else {
+        return -1;
+      }
+      if (bscale != 1.0) {
+        for (int64_t q = 0; q < m[j]; ++q) b[o + q] *= bscale;
+        bound_m[j] *= bscale;
+      }
+      if (perm) {
+        const lp2d::permutation pm =
+            lp2d::shuffle(static_cast<std::size_t>(m[j]), lp2d::derive_seed(seed, 2 * g + 1));
+        std::memcpy(perm + o, pm.order.data(), sizeof(uint32_t) * pm.order.size());
+      }
+    }
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// Config 4 sizes: m = clamp(floor(xmin / u^(1/alpha)), xmin,
+// xmax) with u from xoshiro256pp(derive_seed(seed, 0xB0)).unit(), until the
+// sizes sum to target_total. Returns the count.
+int64_t ref_pareto_sizes(uint64_t seed, double xmin, double alpha, int32_t xmax,
+                         int64_t target_total, int64_t n_max, int32_t* m) {
+  lp2d::xoshiro256pp r(lp2d::derive_seed(seed, 0xB0));
+  int64_t total = 0, n = 0;
+  while (n < n_max && total < target_total) {
+    const double u = r.unit();
+    double v = u > 0.0 ? std::floor(xmin / std::pow(u, 1.0 / alpha)) : (double)xmax;
+    v = std::min<double>(v, xmax);
+    v = std::max<double>(v, xmin);
+    m[n] = static_cast<int32_t>(v);
+    total += m[n];
+    ++n;
+  }
+  return n;
 }
 
 // serial.hpp solve on one LP, with stats.

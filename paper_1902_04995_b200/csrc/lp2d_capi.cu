@@ -517,10 +517,63 @@ KParams make_params(const lp2d_opts* o) {
   return kp;
 }
 
+// fp32 storage: widen the batch's scalars into double copies on the device
+// (k_widen), the input of the double kernels for those classes. kp's scalar
+// pointers are redirected to the copies carved from ws (5 arrays).
+size_t widen_bytes(int64_t E, int64_t n) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  return 3 * al(sizeof(double) * E) + al(sizeof(double) * 2 * n) + al(sizeof(double) * n);
+}
+
+int widen_batch(KParams& kp, int64_t E, int64_t n, char* ws, int dev, cudaStream_t s) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const void* src[5] = {kp.ax, kp.ay, kp.b, kp.c, kp.bound_m};
+  const int64_t cnt[5] = {E, E, E, 2 * n, n};
+  void* dst[5];
+  size_t o = 0;
+  for (int k = 0; k < 5; ++k) {
+    dst[k] = ws + o;
+    o += al(sizeof(double) * cnt[k]);
+    if (cnt[k] == 0) continue;
+    const int threads = 256;
+    const int64_t want = (cnt[k] / 4 + threads - 1) / threads;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)g_dev[dev].sm_count * 8));
+    k_widen<<<grid, threads, 0, s>>>(cnt[k], static_cast<const float*>(src[k]),
+                                     static_cast<double*>(dst[k]));
+    note_launch();
+  }
+  CUDA_TRY(cudaGetLastError());
+  kp.ax = dst[0];
+  kp.ay = dst[1];
+  kp.b = dst[2];
+  kp.c = dst[3];
+  kp.bound_m = dst[4];
+  return 0;
+}
+
+// Solve of a device-resident batch with scalars stored as S (float or
+// double); the arithmetic is the reference's double in both cases and the
+// outputs are double. E = scalar elements (offset[n]).
+template <typename S>
+int solve_device_batch(KParams kp, int64_t E, int64_t min_m, int64_t max_m, int perm_bits,
+                       int sched, int dev, cudaStream_t s, bool may_sync) {
+  if constexpr (sizeof(S) == 4) {
+    void* ws = nullptr;
+    CUDA_TRY(cudaMallocFromPoolAsync(&ws, widen_bytes(E, kp.n_list), g_dev[dev].pool, s));
+    int rc = widen_batch(kp, E, kp.n_list, static_cast<char*>(ws), dev, s);
+    if (rc == 0) rc = launch_solve<double>(kp, min_m, max_m, perm_bits, sched, dev, s, may_sync);
+    CUDA_TRY(cudaFreeAsync(ws, s));
+    return rc;
+  } else {
+    return launch_solve<double>(kp, min_m, max_m, perm_bits, sched, dev, s, may_sync);
+  }
+}
+
 // ---- host mode: one shard [lo, hi) on one device ----------------------------
-template <typename T>
+template <typename S>
 int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out,
                      int64_t lo, int64_t hi, int64_t min_m, int64_t max_m) {
+  using T = double;  // outputs
   if (int rc = ensure_device(dev)) return rc;
   DeviceState& d = g_dev[dev];
   std::lock_guard<std::mutex> lock(d.mu);
@@ -533,12 +586,12 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   size_t off_m = 0;
   size_t off_offset = off_m + al(sizeof(int32_t) * cnt);
   size_t off_ax = off_offset + al(sizeof(int64_t) * (cnt + 1));
-  size_t off_ay = off_ax + al(sizeof(T) * E);
-  size_t off_b = off_ay + al(sizeof(T) * E);
-  size_t off_perm = off_b + al(sizeof(T) * E);
+  size_t off_ay = off_ax + al(sizeof(S) * E);
+  size_t off_b = off_ay + al(sizeof(S) * E);
+  size_t off_perm = off_b + al(sizeof(S) * E);
   size_t off_c = off_perm + al(ps * E);
-  size_t off_M = off_c + al(sizeof(T) * 2 * cnt);
-  size_t off_st = off_M + al(sizeof(T) * cnt);
+  size_t off_M = off_c + al(sizeof(S) * 2 * cnt);
+  size_t off_st = off_M + al(sizeof(S) * cnt);
   size_t off_x = off_st + al(cnt);
   size_t off_y = off_x + al(sizeof(T) * cnt);
   size_t off_v = off_y + al(sizeof(T) * cnt);
@@ -560,17 +613,17 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   CUDA_TRY(cudaMemcpyAsync(A + off_m, b->m + lo, sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(A + off_offset, offs.data(), sizeof(int64_t) * (cnt + 1),
                            cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(A + off_ax, static_cast<const T*>(b->ax) + e0, sizeof(T) * E,
+  CUDA_TRY(cudaMemcpyAsync(A + off_ax, static_cast<const S*>(b->ax) + e0, sizeof(S) * E,
                            cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(A + off_ay, static_cast<const T*>(b->ay) + e0, sizeof(T) * E,
+  CUDA_TRY(cudaMemcpyAsync(A + off_ay, static_cast<const S*>(b->ay) + e0, sizeof(S) * E,
                            cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(A + off_b, static_cast<const T*>(b->b) + e0, sizeof(T) * E,
+  CUDA_TRY(cudaMemcpyAsync(A + off_b, static_cast<const S*>(b->b) + e0, sizeof(S) * E,
                            cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(A + off_perm, static_cast<const char*>(b->perm) + ps * e0, ps * E,
                            cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(A + off_c, static_cast<const T*>(b->c) + 2 * lo, sizeof(T) * 2 * cnt,
+  CUDA_TRY(cudaMemcpyAsync(A + off_c, static_cast<const S*>(b->c) + 2 * lo, sizeof(S) * 2 * cnt,
                            cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(A + off_M, static_cast<const T*>(b->bound_m) + lo, sizeof(T) * cnt,
+  CUDA_TRY(cudaMemcpyAsync(A + off_M, static_cast<const S*>(b->bound_m) + lo, sizeof(S) * cnt,
                            cudaMemcpyHostToDevice, s));
   KParams kp = make_params<T>(o);
   kp.n_list = cnt;
@@ -590,7 +643,7 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   kp.pair = reinterpret_cast<int32_t*>(A + off_pair);
   kp.viol = reinterpret_cast<uint32_t*>(A + off_viol);
   kp.wu = reinterpret_cast<uint64_t*>(A + off_wu);
-  if (int rc = launch_solve<T>(kp, min_m, max_m, b->perm_bits, o->scheduler, dev, s, true))
+  if (int rc = solve_device_batch<S>(kp, E, min_m, max_m, b->perm_bits, o->scheduler, dev, s, true))
     return rc;
   CUDA_TRY(cudaMemcpyAsync(out->status + lo, A + off_st, cnt, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(static_cast<T*>(out->x) + lo, A + off_x, sizeof(T) * cnt,
@@ -612,7 +665,7 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   return 0;
 }
 
-template <typename T>
+template <typename S>
 int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
   if (int rc = validate_common(b, o, out)) return rc;
   DeviceGuard guard;
@@ -624,10 +677,10 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
     if (b->perm_bits == 16 && b->max_m > 65536)
       return fail(LP2D_ERR_ARG, "u16 permutations need m <= 65536");
     const int dev = o->device;
-    if (dev < 0 || dev >= ndev) return fail(LP2D_ERR_ARG, "bad device ordinal");
+    if (dev < 0 || dev >= ndev || dev >= 64) return fail(LP2D_ERR_ARG, "bad device ordinal");
     if (int rc = ensure_device(dev)) return rc;
     CUDA_TRY(cudaSetDevice(dev));
-    KParams kp = make_params<T>(o);
+    KParams kp = make_params<double>(o);
     kp.n_list = b->n;
     kp.m = b->m;
     kp.offset = b->offset;
@@ -644,8 +697,12 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
     kp.pair = out->pair;
     kp.viol = out->violation_events;
     kp.wu = out->work_units;
-    return launch_solve<T>(kp, b->min_m, b->max_m, b->perm_bits, o->scheduler, dev,
-                           static_cast<cudaStream_t>(o->stream));
+    int64_t E = 0;  // scalar elements (offset[n]), needed to widen fp32 storage
+    if constexpr (sizeof(S) == 4) {
+      CUDA_TRY(cudaMemcpy(&E, b->offset + b->n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    }
+    return solve_device_batch<S>(kp, E, b->min_m, b->max_m, b->perm_bits, o->scheduler, dev,
+                                 static_cast<cudaStream_t>(o->stream), false);
   }
   // host mode: validate the layout contract, then shard.
   int64_t max_m = 0, min_m = INT64_MAX;
@@ -662,16 +719,16 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
   if (b->perm_bits == 16 && max_m > 65536)
     return fail(LP2D_ERR_ARG, "u16 permutations need m <= 65536");
   int use = o->n_gpus > 0 ? std::min(o->n_gpus, ndev) : ndev;
-  use = (int)std::min<int64_t>(use, b->n);
+  use = (int)std::min<int64_t>(std::min(use, 64), b->n);
   std::vector<int64_t> cut(use + 1, 0);
   lp2dgpu_partition(b->n, b->m, use, cut.data());
-  if (use == 1) return solve_shard_host<T>(0, b, o, out, 0, b->n, min_m, max_m);
+  if (use == 1) return solve_shard_host<S>(0, b, o, out, 0, b->n, min_m, max_m);
   std::vector<int> rcs(use, 0);
   std::vector<std::string> errs(use);
   std::vector<std::thread> th;
   for (int g = 0; g < use; ++g) {
     th.emplace_back([&, g] {
-      if (cut[g + 1] > cut[g]) rcs[g] = solve_shard_host<T>(g, b, o, out, cut[g], cut[g + 1], min_m, max_m);
+      if (cut[g + 1] > cut[g]) rcs[g] = solve_shard_host<S>(g, b, o, out, cut[g], cut[g + 1], min_m, max_m);
       if (rcs[g]) errs[g] = g_err;
     });
   }

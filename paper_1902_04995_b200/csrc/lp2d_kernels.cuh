@@ -1373,6 +1373,30 @@ __global__ void k_bin_scatter(int64_t n, const int32_t* m, BinSpec spec, const i
   }
 }
 
+// fp32-stored batches are solved with the reference's double arithmetic
+// (the fp32 configs' semantics: the reference applied to the fp32-rounded
+// instance). Every float is exactly a double, so widening is exact; this is
+// the staging step for the size classes without an fp32-storage kernel.
+__global__ void k_widen(int64_t n, const float* __restrict__ in, double* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n4 = n / 4;
+  const float4* in4 = reinterpret_cast<const float4*>(in);
+  double2* out2 = reinterpret_cast<double2*>(out);
+  const bool vec = ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec) {
+    for (int64_t i = i0; i < n4; i += stride) {
+      const float4 v = __ldcs(in4 + i);
+      __stcs(out2 + 2 * i, make_double2((double)v.x, (double)v.y));
+      __stcs(out2 + 2 * i + 1, make_double2((double)v.z, (double)v.w));
+    }
+    for (int64_t i = 4 * n4 + i0; i < n; i += stride) out[i] = (double)in[i];
+  } else {
+    for (int64_t i = i0; i < n; i += stride) out[i] = (double)in[i];
+  }
+}
+
 // K1: device Fisher-Yates (serial.hpp:138-146), one thread per LP, in place.
 template <typename P>
 __global__ void k_shuffle(int64_t n, const int32_t* m, const int64_t* offset,

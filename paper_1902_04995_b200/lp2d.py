@@ -11,10 +11,12 @@ Reference interface (paths under /root/reference/proj/include/lp2d/):
   gen / gen_mixed      generate.hpp:143-189  -> gen(), gen_mixed()
 
 solve_batch raises ValueError exactly where the reference throws
-std::invalid_argument (batch.hpp:306-320). Solutions compare equal to the
-reference's for fp64 (value equality of x, y, value and the feasibility flag);
-the builder's extensions (status incl. "unbounded", the defining constraint
-pair, per-LP violation/work-unit counts) ride along.
+std::invalid_argument (batch.hpp:306-320). Scalars may be stored as float64 or
+float32; either way the arithmetic is the reference's double arithmetic and
+the results (double) compare equal to the reference's on the stored instance
+(value equality of x, y, value and the feasibility flag). The builder's
+extensions (status incl. "unbounded", the defining constraint pair, per-LP
+violation/work-unit counts) ride along.
 
 For throughput, PackedBatch keeps the structure-of-arrays layout the kernels
 consume and solve_packed() runs on host or device (torch) buffers.
@@ -356,8 +358,9 @@ def solve_packed(pb: PackedBatch, cfg: BlockConfig = BlockConfig(), tol: Toleran
     arrs = [np.ascontiguousarray(a) for a in (pb.m, pb.offset, pb.ax, pb.ay, pb.b, pb.perm, pb.c, pb.M)]
     m, off, ax, ay, b, perm, c, M = arrs
     if out is None:
-        out = PackedResult(np.zeros(pb.n, np.uint8), np.zeros(pb.n, dt), np.zeros(pb.n, dt),
-                           np.zeros(pb.n, dt), np.zeros((pb.n, 2), np.int32),
+        # results are the reference's doubles for both storage types
+        out = PackedResult(np.zeros(pb.n, np.uint8), np.zeros(pb.n), np.zeros(pb.n),
+                           np.zeros(pb.n), np.zeros((pb.n, 2), np.int32),
                            np.zeros(pb.n, np.uint32), np.zeros(pb.n, np.uint64))
     s = N.BatchSoA(pb.n, m.ctypes.data, off.ctypes.data, ax.ctypes.data, ay.ctypes.data,
                    b.ctypes.data, perm.ctypes.data, 16 if perm.dtype == np.uint16 else 32,
@@ -450,7 +453,7 @@ class DeviceBatch:
         import torch
 
         dev = torch.device("cuda", self.device)
-        tdt = torch.float32 if self.dtype == np.float32 else torch.float64
+        tdt = torch.float64  # results are the reference's doubles for both storage types
         n = self.n
         return PackedResult(torch.zeros(n, dtype=torch.uint8, device=dev),
                             torch.zeros(n, dtype=tdt, device=dev), torch.zeros(n, dtype=tdt, device=dev),

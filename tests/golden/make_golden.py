@@ -11,10 +11,13 @@ Fixtures (all small):
   ref_<name>.npz    reference fp64 results (feasible, x, y, value, per-LP
                     violation_events and work_units from serial solve with
                     solve_stats) for the instance batches below.
+  ref32_<name>.npz  the same reference results for the fp32-rounded copy of
+                    each batch (the fp32 configs: float storage, the
+                    reference's double arithmetic on the widened values).
   oracle_<name>.npz the restated oracle's status / defining pair for the same
                     batches (fp64) and for their fp32-rounded copies — the
-                    builder extension and fp32 have no reference counterpart,
-                    so these pin the restatement against regressions.
+                    builder extension has no reference counterpart, so these
+                    pin the restatement against regressions.
 """
 from __future__ import annotations
 
@@ -172,6 +175,8 @@ def main():
         np.savez_compressed(os.path.join(HERE, f"batch_{name}.npz"), m=pk.m, offset=pk.offset,
                             ax=pk.ax, ay=pk.ay, b=pk.b, perm=pk.perm, c=pk.c, M=pk.M)
         np.savez_compressed(os.path.join(HERE, f"ref_{name}.npz"), **ref_results(pk))
+        np.savez_compressed(os.path.join(HERE, f"ref32_{name}.npz"),
+                            **ref_results(pk.astype(np.float32).astype(np.float64)))
         o64 = O.solve_batch(pk)
         o32 = O.solve_batch(pk.astype(np.float32))
         np.savez_compressed(os.path.join(HERE, f"oracle_{name}.npz"),

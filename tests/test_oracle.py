@@ -123,3 +123,21 @@ def test_reference_gen_mixed_kats(O):
     k = KAT["gen_mixed_64_1024_1"]
     assert k["violation_events"] == 7227 and k["total_wu"] == 147079
     assert k["checksum"] == pytest.approx(16797174.362085555, rel=1e-15)
+
+
+@pytest.mark.parametrize("name", ["c1", "mixed", "verify", "m1024"])
+def test_fp32_oracle_is_reference_on_rounded_instance(O, name):
+    """fp32 configs: float storage, the reference's double arithmetic. The
+    oracle's float entry point == the unmodified reference run on the
+    fp32-rounded instance (widened to double), bit for bit incl. stats."""
+    pk = load_batch(name).astype(np.float32)
+    ref = load_npz(f"ref32_{name}.npz")
+    o = O.solve_batch(pk)
+    feas = o["status"] != O.INFEASIBLE
+    assert np.array_equal(feas, ref["feasible"].astype(bool))
+    for k in ("x", "y", "value"):
+        assert np.array_equal(o[k][feas], ref[k][feas]), k
+    assert np.array_equal(o["violation_events"], ref["violation_events"])
+    assert np.array_equal(o["work_units"], ref["work_units"])
+    g = load_npz(f"oracle_{name}.npz")
+    assert np.array_equal(o["status"], g["status32"]) and np.array_equal(o["pair"], g["pair32"])
