@@ -178,6 +178,14 @@ int lp2dgpu_segmented_extremes(const double* in, int64_t n, int64_t contention,
                                int32_t strategy, double* out_min, double* out_max,
                                int32_t device, void* stream);
 
+/* Measurement hook of the fp32-storage kernel (K4): with the environment
+ * variable LP2D_B200_FX_STATS=1 the kernels count events, first-pass
+ * certificates, frame shifts, exact (double) events, uncertain tests, lazy
+ * exact optima, whole-LP exact solves (8 counters, summed over calls).
+ * Copies them into out[0..7] (reset if reset != 0) and returns 8, or 0 when
+ * counting is off. */
+int lp2dgpu_fx_stats(uint64_t* out, int reset);
+
 /* Number of visible CUDA devices (0 when none). */
 int lp2dgpu_device_count(void);
 

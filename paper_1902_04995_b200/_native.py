@@ -88,6 +88,7 @@ EXPORTS = (
     "lp2dgpu_shuffle_device",
     "lp2dgpu_generate_device",
     "lp2dgpu_device_count",
+    "lp2dgpu_fx_stats",
     "lp2dgpu_kernel_launches",
     "lp2dgpu_segmented_extremes",
     "lp2dgpu_last_error",
@@ -140,6 +141,8 @@ def lib():
                                           C.c_int32, C.c_void_p]
     L.lp2dgpu_generate_device.restype = C.c_int
     L.lp2dgpu_device_count.restype = C.c_int
+    L.lp2dgpu_fx_stats.argtypes = [C.c_void_p, C.c_int]
+    L.lp2dgpu_fx_stats.restype = C.c_int
     L.lp2dgpu_kernel_launches.restype = C.c_uint64
     L.lp2dgpu_segmented_extremes.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int32,
                                              C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]

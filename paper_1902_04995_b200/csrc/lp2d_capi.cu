@@ -360,12 +360,117 @@ int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t ma
 // may_sync: host mode (which synchronises anyway) reads the class counts back
 // and launches only the non-empty classes with right-sized grids; device
 // mode stays asynchronous and launches every class in [min_m, max_m].
+// ---- fp32 storage: K4 (k_solve_fx, lp2d_fx.cuh) for the warp classes ------
+// Same staging geometry and CTA-shape selection as the double/float warp
+// kernels (WarpLayout<float, ...>): register-only classes at a compile-time
+// CTA shape, late-TMA classes at the run-time shape with the most resident
+// warps.
+template <typename P, int NS, int NT, int CAP>
+int launch_fx_cap(KParams kp, int dev, cudaStream_t stream) {
+  using L = WarpLayout<float, P, NS, NT, CAP>;
+  auto kern = k_solve_fx<P, NS, NT, CAP>;
+  struct Shape {
+    int warps = 0, blocks = 0;
+  };
+  static Shape shape[64];
+  static std::mutex mu;
+  Shape sh;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!shape[dev].warps) {
+      Shape best;
+      if constexpr (L::kLateTma) {
+        int optin = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+        for (int w = 1; w <= L::kMaxWarpsRt; ++w) {
+          int b = 0;
+          CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, w * 32,
+                                                                 (size_t)w * (L::kBuf + 8)));
+          if (b * w > best.blocks * best.warps) best = Shape{w, b};
+        }
+      } else {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)L::kSmem));
+        int b = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, L::kWarps * 32, L::kSmem));
+        best = Shape{L::kWarps, b};
+      }
+      if (best.blocks < 1) return fail(LP2D_ERR_CUDA, "fx warp kernel does not fit on an SM");
+      shape[dev] = best;
+    }
+    sh = shape[dev];
+  }
+  const size_t smem = L::kLateTma ? (size_t)sh.warps * (L::kBuf + 8) : (size_t)L::kSmem;
+  const int64_t want = (kp.n_list + sh.warps - 1) / sh.warps;
+  const int64_t maxb = (int64_t)sh.blocks * g_dev[dev].sm_count;
+  const int grid = (int)std::max<int64_t>(1, std::min(want, maxb));
+  kp.total_warps = grid * sh.warps;
+  kp.counter = take_counter(dev);
+  kern<<<grid, sh.warps * 32, smem, stream>>>(kp);
+  note_launch();
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <typename P, int NS, int NT>
+int launch_fx(KParams kp, int64_t max_m, int dev, cudaStream_t s) {
+  if constexpr (NS + NT == 33) {
+    if (max_m > 0 && max_m <= 1024) return launch_fx_cap<P, NS, NT, 1024>(kp, dev, s);
+  }
+  return launch_fx_cap<P, NS, NT, 0>(kp, dev, s);
+}
+
+#ifndef LP2D_FX_NS33
+#define LP2D_FX_NS33 8  // register chunks of the m <= 1052 class (config 2)
+#endif
+
+// K4 covers the warp classes (29 <= m <= 4124); the lane class and the CTA
+// class read widened double copies (LP2D_B200_FX=0: every class does, A/B).
+bool fx_class(int cls) {
+  static const bool on = !(std::getenv("LP2D_B200_FX") && std::getenv("LP2D_B200_FX")[0] == '0');
+  return on && cls >= 1 && cls < n_reg_classes<double>();
+}
+
+template <typename P>
+int launch_fx_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t max_m) {
+  switch (kSlotClasses[cls]) {
+    case 2: return launch_fx<P, 2, 0>(kp, max_m, dev, s);
+    case 4: return launch_fx<P, 4, 0>(kp, max_m, dev, s);
+    case 5: return launch_fx<P, 5, 0>(kp, max_m, dev, s);
+    case 6: return launch_fx<P, 6, 0>(kp, max_m, dev, s);
+    case 9: return launch_fx<P, 9, 0>(kp, max_m, dev, s);
+    case 10: return launch_fx<P, 10, 0>(kp, max_m, dev, s);
+    case 18: return launch_fx<P, 10, 8>(kp, max_m, dev, s);
+    case 33: return launch_fx<P, LP2D_FX_NS33, 33 - LP2D_FX_NS33>(kp, max_m, dev, s);
+    case 65: return launch_fx<P, 16, 49>(kp, max_m, dev, s);
+    case 129: return launch_fx<P, 16, 113>(kp, max_m, dev, s);
+  }
+  return fail(LP2D_ERR_UNSUPPORTED, "fx size class not built");
+}
+
+template <typename T, typename F>
+int launch_binned(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStream_t s,
+                  bool may_sync, F&& launch_cls);
+
 template <typename T, typename P>
 int launch_balanced(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStream_t s,
                     bool may_sync) {
+  return launch_binned<T>(kp, min_m, max_m, dev, s, may_sync,
+                          [](const KParams& kc, int c, int d, cudaStream_t cs, int64_t cap_m) {
+                            return launch_class<T, P>(kc, c, d, cs, cap_m);
+                          });
+}
+
+// Size-class dispatch: a uniform batch is one launch; a mixed batch is binned
+// on the device and launched one class per stream. launch_cls(kp, class, dev,
+// stream, max_m) launches one class.
+template <typename T, typename F>
+int launch_binned(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStream_t s,
+                  bool may_sync, F&& launch_cls) {
   const int cmin = class_of<T>(std::max<int64_t>(min_m, 0));
   const int cmax = class_of<T>(max_m);
-  if (cmin == cmax) return launch_class<T, P>(kp, cmax, dev, s, max_m);
+  if (cmin == cmax) return launch_cls(kp, cmax, dev, s, max_m);
   // Mixed sizes: bin LP ids by class on the device, one launch per class.
   BinSpec spec{};
   spec.nreg = n_reg_classes<T>();
@@ -440,7 +545,7 @@ int launch_balanced(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStrea
       if (may_sync) kc.n_list = n_host;
       cudaStream_t cs = d.cls_stream[sidx];
       CUDA_TRY(cudaStreamWaitEvent(cs, d.cls_event[16], 0));
-      int r = launch_class<T, P>(kc, c, dev, cs, cap_m);
+      int r = launch_cls(kc, c, dev, cs, cap_m);
       CUDA_TRY(cudaEventRecord(d.cls_event[sidx], cs));
       CUDA_TRY(cudaStreamWaitEvent(s, d.cls_event[sidx], 0));
       return r;
@@ -502,6 +607,19 @@ int validate_common(const lp2d_batch_soa* b, const lp2d_opts* o, const lp2d_out*
   return 0;
 }
 
+// K4 path counters (LP2D_B200_FX_STATS=1): a device buffer of kFxNStat
+// counters on device 0, read back by lp2dgpu_fx_stats.
+unsigned long long* g_fxstat = nullptr;
+unsigned long long* fx_stats_ptr() {
+  static const bool on = std::getenv("LP2D_B200_FX_STATS") && std::getenv("LP2D_B200_FX_STATS")[0] == '1';
+  if (!on) return nullptr;
+  if (!g_fxstat) {
+    if (cudaMalloc(&g_fxstat, sizeof(unsigned long long) * kFxNStat) != cudaSuccess) return nullptr;
+    cudaMemset(g_fxstat, 0, sizeof(unsigned long long) * kFxNStat);
+  }
+  return g_fxstat;
+}
+
 template <typename T>
 KParams make_params(const lp2d_opts* o) {
   KParams kp{};
@@ -514,6 +632,19 @@ KParams make_params(const lp2d_opts* o) {
   kp.pk.nz = 0x8000000080000000ull;    // (-0.f, -0.f)
   kp.pk.one = 0x3f8000003f800000ull;   // (1.f, 1.f)
   kp.pk.zero = 0;                      // (+0.f, +0.f)
+  kp.fxstat = fx_stats_ptr();
+  {
+    // K4 certificate factors (lp2d_fx.cuh / DESIGN.md §3): u = 2^-24 (fp32),
+    // U = 2^-53 (fp64), rho = 2^-21 (MUFU rcp/rsqrt relative error bound),
+    // ed = rho + 3u + 3U (error of the fp32 line direction); the tolerances
+    // rounded up to float.
+    const double u = 0x1p-24, U = 0x1p-53, rho = 0x1p-21, ed = rho + 3 * u + 3 * U;
+    const double ep = (double)(float)o->eps_parallel * (1 + 0x1p-20);
+    kp.fx_ka = (float)(1.25 * (2 * ed + 2 * (rho + u) + 8 * u + 5 * U) * (1 + 0x1p-20));
+    kp.fx_tp = (float)((16 * (ed + 2 * u) + 3 * ep) * (1 + 0x1p-20) + 0x1p-100);
+    kp.fx_ec = (float)((1.25 * (2 * ed + 2 * u) + 1.02 * ep) * (1 + 0x1p-20));
+    kp.fx_eps = (float)o->eps_feas * (1.0f + 0x1p-20f);
+  }
   return kp;
 }
 
@@ -554,10 +685,43 @@ int widen_batch(KParams& kp, int64_t E, int64_t n, char* ws, int dev, cudaStream
 // Solve of a device-resident batch with scalars stored as S (float or
 // double); the arithmetic is the reference's double in both cases and the
 // outputs are double. E = scalar elements (offset[n]).
+template <typename P>
+int solve_f32_balanced(KParams kp, int64_t E, int64_t min_m, int64_t max_m, int dev,
+                       cudaStream_t s, bool may_sync) {
+  const int cmin = class_of<double>(std::max<int64_t>(min_m, 0));
+  const int cmax = class_of<double>(max_m);
+  bool need_widen = false;
+  for (int c = cmin; c <= cmax; ++c) need_widen |= !fx_class(c);
+  KParams kd = kp;
+  void* ws = nullptr;
+  if (need_widen) {
+    CUDA_TRY(cudaMallocFromPoolAsync(&ws, widen_bytes(E, kp.n_list), g_dev[dev].pool, s));
+    if (int rc = widen_batch(kd, E, kp.n_list, static_cast<char*>(ws), dev, s)) return rc;
+  }
+  const int rc = launch_binned<double>(
+      kp, min_m, max_m, dev, s, may_sync,
+      [&](const KParams& kc, int c, int d, cudaStream_t cs, int64_t cap_m) {
+        if (fx_class(c)) return launch_fx_class<P>(kc, c, d, cs, cap_m);
+        KParams k2 = kc;
+        k2.ax = kd.ax;
+        k2.ay = kd.ay;
+        k2.b = kd.b;
+        k2.c = kd.c;
+        k2.bound_m = kd.bound_m;
+        return launch_class<double, P>(k2, c, d, cs, cap_m);
+      });
+  if (ws) CUDA_TRY(cudaFreeAsync(ws, s));
+  return rc;
+}
+
 template <typename S>
 int solve_device_batch(KParams kp, int64_t E, int64_t min_m, int64_t max_m, int perm_bits,
                        int sched, int dev, cudaStream_t s, bool may_sync) {
   if constexpr (sizeof(S) == 4) {
+    if (sched == LP2D_SCHED_BALANCED) {
+      if (perm_bits == 16) return solve_f32_balanced<uint16_t>(kp, E, min_m, max_m, dev, s, may_sync);
+      return solve_f32_balanced<uint32_t>(kp, E, min_m, max_m, dev, s, may_sync);
+    }
     void* ws = nullptr;
     CUDA_TRY(cudaMallocFromPoolAsync(&ws, widen_bytes(E, kp.n_list), g_dev[dev].pool, s));
     int rc = widen_batch(kp, E, kp.n_list, static_cast<char*>(ws), dev, s);
@@ -925,6 +1089,17 @@ int lp2dgpu_segmented_extremes(const double* in, int64_t n, int64_t contention, 
   }
   CUDA_TRY(cudaGetLastError());
   return 0;
+}
+
+// Debug/measurement: copy (and optionally reset) the K4 path counters
+// (enabled by LP2D_B200_FX_STATS=1; returns the counter count, 0 if off).
+int lp2dgpu_fx_stats(uint64_t* out, int reset) {
+  if (!g_fxstat) return 0;
+  if (cudaMemcpy(out, g_fxstat, sizeof(unsigned long long) * kFxNStat, cudaMemcpyDeviceToHost) !=
+      cudaSuccess)
+    return 0;
+  if (reset) cudaMemset(g_fxstat, 0, sizeof(unsigned long long) * kFxNStat);
+  return kFxNStat;
 }
 
 int lp2dgpu_device_count(void) {

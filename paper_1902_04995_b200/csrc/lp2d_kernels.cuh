@@ -65,6 +65,10 @@ struct KParams {
   float eps_par_f, eps_feas_f, eps_hi_f;  // (float copies: constant-bank operands)
   int32_t total_warps;
   PairConsts pk;  // packed-fp32 constants (lp2d_pair.cuh)
+  unsigned long long* fxstat;  // K4 path counters (LP2D_B200_FX_STATS; null normally)
+  // K4 certificate factors (host-computed from the tolerance, lp2d_fx.cuh):
+  // Ka = A*fx_ka, Tpar = A*fx_tp, Ec = (|cx|+|cy|)*fx_ec, eps_feas rounded up
+  float fx_ka, fx_tp, fx_ec, fx_eps;
 };
 
 template <typename T>
@@ -399,14 +403,16 @@ __device__ __forceinline__ void write_result(const KParams& p,
 // memory with the reference's classify (wu_apply). Taken only when a unit of
 // the register fold hit the parallel bound (essentially parallel constraints),
 // so speed is irrelevant; out of line to keep the hot code small.
-template <typename T, typename P>
+// S: the storage type of the scalars (float storage is widened exactly, the
+// fp32 configs' semantics).
+template <typename T, typename P, typename S = T>
 __device__ __noinline__ Acc<T> fold_exact_global(const KParams& p, int64_t off,
                                                  uint32_t pi, Line<T> l, T M,
                                                  T eps_par, T eps_feas, T eps_hi) {
   const int lane = threadIdx.x & 31;
-  const T* ax = static_cast<const T*>(p.ax) + off;
-  const T* ay = static_cast<const T*>(p.ay) + off;
-  const T* b = static_cast<const T*>(p.b) + off;
+  const S* ax = static_cast<const S*>(p.ax) + off;
+  const S* ay = static_cast<const S*>(p.ay) + off;
+  const S* b = static_cast<const S*>(p.b) + off;
   const P* perm = static_cast<const P*>(p.perm) + off;
   Acc<T> acc;
   acc.uL = -T(INFINITY);
@@ -420,9 +426,9 @@ __device__ __noinline__ Acc<T> fold_exact_global(const KParams& p, int64_t off,
       vb = M;
     } else {
       const uint32_t o = perm[k - 4];
-      vax = ax[o];
-      vay = ay[o];
-      vb = b[o];
+      vax = (T)ax[o];
+      vay = (T)ay[o];
+      vb = (T)b[o];
     }
     wu_apply(vax, vay, vb, l, eps_par, eps_feas, eps_hi, k, acc);
   }
@@ -513,14 +519,14 @@ __device__ __forceinline__ bool resolve_event(LPState<T>& S, const Acc<T>& acc,
 // the reference loop with warp-parallel tests and folds. Used for LPs whose
 // magnitudes leave the fast path's proven range (non-finite or huge
 // coefficients, a non-finite running optimum); rare, so simple.
-template <typename T, typename P>
+template <typename T, typename P, typename SS = T>
 __device__ __noinline__ void solve_exact_global(const KParams& p, const Header<T>& h,
                                                 T eps_par, T eps_feas, T eps_hi,
                                                 LPState<T>& S) {
   const int lane = threadIdx.x & 31;
-  const T* ax = static_cast<const T*>(p.ax) + h.off;
-  const T* ay = static_cast<const T*>(p.ay) + h.off;
-  const T* b = static_cast<const T*>(p.b) + h.off;
+  const SS* ax = static_cast<const SS*>(p.ax) + h.off;
+  const SS* ay = static_cast<const SS*>(p.ay) + h.off;
+  const SS* b = static_cast<const SS*>(p.b) + h.off;
   const P* perm = static_cast<const P*>(p.perm) + h.off;
   lp_init(S, h);
   const T cthr = eps_par * sqrt(h.cx * h.cx + h.cy * h.cy);
@@ -531,7 +537,7 @@ __device__ __noinline__ void solve_exact_global(const KParams& p, const Header<T
     bool v = false;
     if (i < m) {
       const uint32_t o = perm[i];
-      v = !satisfied(ax[o], ay[o], b[o], S.px, S.py, eps_feas);
+      v = !satisfied((T)ax[o], (T)ay[o], (T)b[o], S.px, S.py, eps_feas);
     }
     const uint32_t vm = __ballot_sync(kFull, v);
     if (!vm) {
@@ -543,8 +549,8 @@ __device__ __noinline__ void solve_exact_global(const KParams& p, const Header<T
     const uint32_t pi = 4u + (uint32_t)iv;
     S.viol += 1;
     S.wu += pi;
-    const Line<T> l = boundary_of(ax[o], ay[o], b[o]);
-    const Acc<T> acc = fold_exact_global<T, P>(p, h.off, pi, l, h.M, eps_par, eps_feas, eps_hi);
+    const Line<T> l = boundary_of((T)ax[o], (T)ay[o], (T)b[o]);
+    const Acc<T> acc = fold_exact_global<T, P, SS>(p, h.off, pi, l, h.M, eps_par, eps_feas, eps_hi);
     if (!resolve_event(S, acc, l, pi, h, cthr, eps_feas)) return;
     start = iv + 1;
   }
@@ -1492,3 +1498,4 @@ __global__ void k_generate(int64_t n, int64_t first, uint64_t seed, const int32_
 }  // namespace lp2d_b200
 
 #include "lp2d_warp.cuh"
+#include "lp2d_fx.cuh"

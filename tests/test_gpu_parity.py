@@ -264,7 +264,9 @@ def test_kernel_launch_counter(P):
     uni = P.DeviceBatch(P.PackedBatch.generate(np.full(512, 200, np.int32), 3).astype(np.float32))
     mixed = P.DeviceBatch(P.PackedBatch.generate(np.array([8, 40, 100, 700, 3000], np.int32)
                                                  .repeat(64), 3).astype(np.float32))
-    for db, lo, hi in ((uni, 1, 1), (mixed, 3, 2 + 11)):  # 2 binning + <= 11 class launches
+    # uniform fp32 warp class: one K4 launch; mixed: 2 binning + 5 widening
+    # (the lane/CTA classes read double copies) + <= 11 class launches
+    for db, lo, hi in ((uni, 1, 1), (mixed, 3, 2 + 5 + 11)):
         out = db.empty_result()
         k0 = P.kernel_launches()
         P.solve_device(db, out)
