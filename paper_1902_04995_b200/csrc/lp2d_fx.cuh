@@ -16,8 +16,8 @@
 //   * local frame: constraints are used as (a, b') with b' = b - a.s for a
 //     per-LP shift s (fp32 point). b' is computed from the original b by fp32
 //     error-free transformations (bshift), so |b'32 - (b - a.s)| <= u|b'| + Eb:
-//     kept in registers for the register chunks, computed on the fly for the
-//     tail (the staging buffer keeps the original values). s starts at 0 and
+//     kept in registers for the register chunks and rewritten in place in the
+//     staging buffer for the tail (originals re-read from L2). s starts at 0 and
 //     is moved (reshift) to the current candidate point when a certificate
 //     fails at an event, so coordinates near the optimum are small and fp32
 //     resolves them.
@@ -146,65 +146,73 @@ __device__ LP2D_FX_COLD void fx_exact_point(double hx, double hy, double hb, dou
   py = l.oy + t * l.dy;
 }
 
-// Fold accumulator of one lane: the chosen side's top two quotients (+ the
-// owner slot of the first), the other side's minimum, min |a.d|.
+// Fold accumulator of one lane, with PER-UNIT error bounds: every unit's
+// quotient q lies within e = (Kn + Ka |q|)/|a.d| of the reference's sigma64 -
+// tau, so it is represented by [lo, hi] = [q - e, q + e]. Chosen side: the
+// two largest hi (and the lo and owner slot of the first); other side: the
+// smallest lo; all units: min |a.d| (parallel / sign certificate).
 struct FxAcc {
-  float h1, h2, r1, mal;
-  float oal;  // |a.d| of the top quotient's unit (its own error bound)
+  float h1, l1, h2, rl, mal;
   uint32_t own;
 };
 
 __device__ __forceinline__ void fx_acc_init(FxAcc& a) {
   a.h1 = -INFINITY;
+  a.l1 = -INFINITY;
   a.h2 = -INFINITY;
-  a.r1 = INFINITY;
+  a.rl = INFINITY;
   a.mal = INFINITY;
-  a.oal = 0.0f;
   a.own = kNone;
 }
 
 // Two work units (classify, core.hpp:96-109, in the local flipped frame):
 // alm = -(a.d'), nmn = -(b' - a.w) = a.w - b' (nb = -b'), q = nmn / alm.
 // Chosen side (d' flipped so it is the max side): a.d' < 0  <=>  alm > 0.
+// kn/ka: the event's numerator error and the LP's quotient error factor
+// (pre-scaled by 1 + 2^-10 for the rounding of e itself).
 template <bool MASKED>
 __device__ __forceinline__ void fx_fold2(Pair<float> ax, Pair<float> ay, Pair<float> nb,
                                          Pair<float> ndx, Pair<float> ndy, Pair<float> wx,
-                                         Pair<float> wy, uint32_t s0, uint32_t s1, bool act0,
-                                         bool act1, FxAcc& a, const PairConsts& k) {
+                                         Pair<float> wy, float kn, float ka, uint32_t s0,
+                                         uint32_t s1, bool act0, bool act1, FxAcc& a,
+                                         const PairConsts& k) {
   const Pair<float> alm = fma2(ax, ndx, mul2(ay, ndy, k));
   const Pair<float> nmn = fma2(ax, wx, fma2(ay, wy, nb));
   const float r0 = rcp_approx(lo2(alm)), r1 = rcp_approx(hi2(alm));
   const Pair<float> q = mul2(nmn, mk2(r0, r1), k);
   const float a0 = lo2(alm), a1 = hi2(alm), q0 = lo2(q), q1 = hi2(q);
+  const float e0 = fmaf(ka, fabsf(q0), kn) * fabsf(r0);
+  const float e1 = fmaf(ka, fabsf(q1), kn) * fabsf(r1);
+  const Pair<float> E = mk2(e0, e1);
+  const Pair<float> hi = add2(q, E), lo = sub2(q, E);
+  const float h0 = lo2(hi), hh1 = hi2(hi), w0 = lo2(lo), w1 = hi2(lo);
   const bool l0 = a0 > 0.0f, l1 = a1 > 0.0f;
-  float qL0, qL1, qR0, qR1, m0 = a0, m1 = a1;
+  float hL0, hL1, lR0, lR1, m0 = a0, m1 = a1;
   if constexpr (MASKED) {
-    qL0 = (act0 & l0) ? q0 : -INFINITY;
-    qL1 = (act1 & l1) ? q1 : -INFINITY;
-    qR0 = (act0 & (a0 < 0.0f)) ? q0 : INFINITY;
-    qR1 = (act1 & (a1 < 0.0f)) ? q1 : INFINITY;
+    hL0 = (act0 & l0) ? h0 : -INFINITY;
+    hL1 = (act1 & l1) ? hh1 : -INFINITY;
+    lR0 = (act0 & (a0 < 0.0f)) ? w0 : INFINITY;
+    lR1 = (act1 & (a1 < 0.0f)) ? w1 : INFINITY;
     m0 = act0 ? m0 : INFINITY;
     m1 = act1 ? m1 : INFINITY;
   } else {
-    qL0 = l0 ? q0 : -INFINITY;
-    qL1 = l1 ? q1 : -INFINITY;
-    qR0 = (a0 < 0.0f) ? q0 : INFINITY;
-    qR1 = (a1 < 0.0f) ? q1 : INFINITY;
+    hL0 = l0 ? h0 : -INFINITY;
+    hL1 = l1 ? hh1 : -INFINITY;
+    lR0 = (a0 < 0.0f) ? w0 : INFINITY;
+    lR1 = (a1 < 0.0f) ? w1 : INFINITY;
   }
   a.mal = min3_abs(a.mal, m0, m1);  // NaN-propagating: a NaN unit fails the certificate
   float rr;
-  asm("min.f32 %0, %1, %2, %3;" : "=f"(rr) : "f"(a.r1), "f"(qR0), "f"(qR1));
-  a.r1 = rr;
-  const float mx = fmaxf(qL0, qL1), mn = fminf(qL0, qL1);
-  const bool first = qL0 >= qL1;
-  const uint32_t om = first ? s0 : s1;
-  const float am = first ? a0 : a1;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(rr) : "f"(a.rl), "f"(lR0), "f"(lR1));
+  a.rl = rr;
+  const float mx = fmaxf(hL0, hL1), mn = fminf(hL0, hL1);
+  const bool first = hL0 >= hL1;
   float h2;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(h2) : "f"(a.h2), "f"(fminf(a.h1, mx)), "f"(mn));
   a.h2 = h2;
   const bool up = mx > a.h1;
-  a.own = up ? om : a.own;
-  a.oal = up ? am : a.oal;
+  a.own = up ? (first ? s0 : s1) : a.own;
+  a.l1 = up ? (first ? w0 : w1) : a.l1;
   a.h1 = fmaxf(a.h1, mx);
 }
 
@@ -264,17 +272,65 @@ __device__ __forceinline__ FxFrame fx_frame(const FxLP& C, float sx, float sy) {
 // memory, fold_exact_global, resolve_merged): returns 1 if the LP turned
 // infeasible, 2 if the new optimum is not finite, else 0 with the exact
 // optimum in (xp, yp) and its defining positions in (pos0, pos1).
+// The reference's fold (classify + apply_bound with owners, wu_apply) over
+// considered positions [0, pi), lane-strided, on the widened original values:
+// the permutation and a from the staging buffer when it is resident (sperm
+// non-null), b (and everything else) from global memory, 8 positions per lane
+// in flight so the loads overlap.
+template <typename P>
+__device__ __forceinline__ Acc<double> fx_fold_exact(const KParams& p, int64_t off, uint32_t pi,
+                                                     const Line<double>& l, double M,
+                                                     const P* sperm, const float* sax,
+                                                     const float* say) {
+  const int lane = threadIdx.x & 31;
+  const float* gx = static_cast<const float*>(p.ax) + off;
+  const float* gy = static_cast<const float*>(p.ay) + off;
+  const float* gb = static_cast<const float*>(p.b) + off;
+  const P* gp = static_cast<const P*>(p.perm) + off;
+  Acc<double> acc;
+  acc.uL = -INFINITY;
+  acc.uR = INFINITY;
+  acc.oL = acc.oR = acc.par = kNone;
+#pragma unroll 1
+  for (uint32_t k0 = lane; k0 < pi; k0 += 32 * 8) {
+    float vx[8], vy[8], vb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t k = k0 + 32 * u;
+      const bool in = k < pi && k >= 4;
+      const uint32_t o = in ? (sperm ? (uint32_t)sperm[k - 4] : (uint32_t)gp[k - 4]) : 0u;
+      vx[u] = in ? (sax ? sax[o] : gx[o]) : 0.0f;
+      vy[u] = in ? (say ? say[o] : gy[o]) : 0.0f;
+      vb[u] = in ? __ldg(gb + o) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t k = k0 + 32 * u;
+      if (k < pi) {
+        double x = vx[u], y = vy[u], bb = vb[u];
+        if (k < 4) {
+          x = k == 0 ? 1.0 : (k == 1 ? -1.0 : 0.0);  // serial.hpp:47-52
+          y = k == 2 ? 1.0 : (k == 3 ? -1.0 : 0.0);
+          bb = M;
+        }
+        wu_apply(x, y, bb, l, p.eps_par, p.eps_feas, p.eps_hi, k, acc);
+      }
+    }
+  }
+  return acc;
+}
+
 template <typename P>
 __device__ LP2D_FX_COLD int fx_exact_event(const KParams& p, int64_t lp, int64_t off, int m,
                                            uint32_t pi, float cxf, float cyf, float Mf,
                                            uint32_t& pos0, uint32_t& pos1, double& xp,
-                                           double& yp) {
+                                           double& yp, const P* sperm, const float* sax,
+                                           const float* say) {
   const double M = Mf;
   double ox, oy, ob;
   fx_orig<P>(p, off, pi, M, ox, oy, ob);
   const Line<double> l = boundary_of(ox, oy, ob);
-  const Acc<double> ex = fold_exact_global<double, P, float>(p, off, pi, l, M, p.eps_par,
-                                                             p.eps_feas, p.eps_hi);
+  const Acc<double> ex = fx_fold_exact<P>(p, off, pi, l, M, sperm, sax, say);
   Header<double> h64;
   h64.lp = lp;
   h64.off = off;
@@ -350,29 +406,30 @@ __device__ __forceinline__ void fx_fold_pairs(const Pair<float> (&rax)[NP],
                                               const Pair<float> (&ray)[NP],
                                               const Pair<float> (&rnb)[NP], Pair<float> ndx,
                                               Pair<float> ndy, Pair<float> wx, Pair<float> wy,
-                                              int s, int rel, FxAcc& a, const PairConsts& k) {
+                                              float kn, float ka, int s, int rel, FxAcc& a,
+                                              const PairConsts& k) {
   if constexpr (J + 1 < NP) {
     if (2 * J + 3 < s) {
-      fx_fold2<false>(rax[J], ray[J], rnb[J], ndx, ndy, wx, wy, 2 * J, 2 * J + 1, true, true, a, k);
-      fx_fold2<false>(rax[J + 1], ray[J + 1], rnb[J + 1], ndx, ndy, wx, wy, 2 * J + 2, 2 * J + 3,
+      fx_fold2<false>(rax[J], ray[J], rnb[J], ndx, ndy, wx, wy, kn, ka, 2 * J, 2 * J + 1, true, true, a, k);
+      fx_fold2<false>(rax[J + 1], ray[J + 1], rnb[J + 1], ndx, ndy, wx, wy, kn, ka, 2 * J + 2, 2 * J + 3,
                       true, true, a, k);
-      fx_fold_pairs<J + 2, NP>(rax, ray, rnb, ndx, ndy, wx, wy, s, rel, a, k);
+      fx_fold_pairs<J + 2, NP>(rax, ray, rnb, ndx, ndy, wx, wy, kn, ka, s, rel, a, k);
     } else if (2 * J + 1 < s) {
       asm volatile("// fx masked pair %0" ::"n"(J + 1));
-      fx_fold2<false>(rax[J], ray[J], rnb[J], ndx, ndy, wx, wy, 2 * J, 2 * J + 1, true, true, a, k);
-      fx_fold2<true>(rax[J + 1], ray[J + 1], rnb[J + 1], ndx, ndy, wx, wy, 2 * J + 2, 2 * J + 3,
+      fx_fold2<false>(rax[J], ray[J], rnb[J], ndx, ndy, wx, wy, kn, ka, 2 * J, 2 * J + 1, true, true, a, k);
+      fx_fold2<true>(rax[J + 1], ray[J + 1], rnb[J + 1], ndx, ndy, wx, wy, kn, ka, 2 * J + 2, 2 * J + 3,
                      64 * J + 64 < rel, 64 * J + 96 < rel, a, k);
     } else {
       asm volatile("// fx masked pair %0" ::"n"(J));
-      fx_fold2<true>(rax[J], ray[J], rnb[J], ndx, ndy, wx, wy, 2 * J, 2 * J + 1, 64 * J < rel,
+      fx_fold2<true>(rax[J], ray[J], rnb[J], ndx, ndy, wx, wy, kn, ka, 2 * J, 2 * J + 1, 64 * J < rel,
                      64 * J + 32 < rel, a, k);
     }
   } else if constexpr (J < NP) {
     if (2 * J + 1 < s) {
-      fx_fold2<false>(rax[J], ray[J], rnb[J], ndx, ndy, wx, wy, 2 * J, 2 * J + 1, true, true, a, k);
+      fx_fold2<false>(rax[J], ray[J], rnb[J], ndx, ndy, wx, wy, kn, ka, 2 * J, 2 * J + 1, true, true, a, k);
     } else {
       asm volatile("// fx masked pair %0" ::"n"(J));
-      fx_fold2<true>(rax[J], ray[J], rnb[J], ndx, ndy, wx, wy, 2 * J, 2 * J + 1, 64 * J < rel,
+      fx_fold2<true>(rax[J], ray[J], rnb[J], ndx, ndy, wx, wy, kn, ka, 2 * J, 2 * J + 1, 64 * J < rel,
                      64 * J + 32 < rel, a, k);
     }
   }
@@ -405,7 +462,7 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + W * bufb) + wic;
   const float* sax = reinterpret_cast<const float*>(buf);
   const float* say = reinterpret_cast<const float*>(buf + arr);
-  const float* sb = reinterpret_cast<const float*>(buf + 2 * arr);  // original b
+  float* sb = reinterpret_cast<float*>(buf + 2 * arr);  // b, after a reshift b' (frame s)
   const P* sperm = reinterpret_cast<const P*>(buf + 3 * arr);
   auto tail_idx = [&](int c, uint32_t lim) -> uint32_t {
     return min((uint32_t)sperm[32 * min(c, NS + NT - 1) + lane - 4], lim);
@@ -436,6 +493,10 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
   while (h.lp >= 0) {
     mbar_wait(bar, phase);
     phase ^= 1u;
+#ifdef LP2D_FX_TIMELINE
+    uint64_t tl0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl0));
+#endif
 
     // ---- gather (frame s = 0: b' = b) -------------------------------------
     Pair<T> rax[NP], ray[NP], rnb[NP];
@@ -519,8 +580,72 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
                       !(fabsf(h.cy) < 0x1p100f) || !(fabsf(h.M) < 0x1p62f);
     const FxLP C = fx_lp_consts(p, A, B, h.cx, h.cy);
     FxFrame F = fx_frame(C, 0.0f, 0.0f);
-    bool shifted = false;  // frame != 0: the tail's b' is computed on the fly
-    Pair<T> SXp = splat2(0.0f), SYp = splat2(0.0f);
+    bool shifted = false;  // frame != 0 (late-TMA classes: the buffer holds b')
+    // Move the frame to s = (nsx, nsy): b' of every constraint (register
+    // chunks, and in place in the staging buffer for the late-TMA classes).
+    auto reshift = [&](float nsx, float nsy) {
+      fx_count(p, kFxReshift, lane);
+      if constexpr (L::kLateTma) {
+        // b' of every staged constraint rewritten in place (original
+        // order): from the staged original b on the first reshift, else
+        // from the original b in global memory (L2: streamed an LP ago)
+        const Pair<T> SX = splat2(nsx), SY = splat2(nsy);
+        const int nv = (mj + 3) >> 2;
+        float4* sb4 = reinterpret_cast<float4*>(sb);
+        const float4* gb4 = reinterpret_cast<const float4*>(static_cast<const float*>(p.b) + h.off);
+#pragma unroll 1
+        for (int g0 = lane; g0 < nv; g0 += 32 * 8) {
+          float4 vb[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int g = g0 + 32 * u;
+            vb[u] = g < nv ? (shifted ? __ldg(gb4 + g) : sb4[g]) : make_float4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int g = g0 + 32 * u;
+            if (g < nv) {
+              const float4 vx = reinterpret_cast<const float4*>(sax)[g];
+              const float4 vy = reinterpret_cast<const float4*>(say)[g];
+              const Pair<T> lo =
+                  bshift2(mk2(vx.x, vx.y), mk2(vy.x, vy.y), mk2(vb[u].x, vb[u].y), SX, SY, pk);
+              const Pair<T> hi =
+                  bshift2(mk2(vx.z, vx.w), mk2(vy.z, vy.w), mk2(vb[u].z, vb[u].w), SX, SY, pk);
+              sb4[g] = make_float4(lo2(lo), hi2(lo), lo2(hi), hi2(hi));
+            }
+          }
+        }
+        __syncwarp();
+        // register chunks from the rewritten buffer (the box: M - (+-s))
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+          T v[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int K = 2 * j + e;
+            const int P_ = 32 * K + lane;
+            const bool valid = K < NS && (K < L::kAlwaysValid || P_ < mpos);
+            const uint32_t o = min((uint32_t)sperm[K == 0 ? max(P_ - 4, 0) : P_ - 4], cap - 1u);
+            v[e] = valid ? -sb[o] : -INFINITY;
+            if (K == 0 && P_ < 4)
+              v[e] = -bshift(P_ == 0 ? 1.0f : (P_ == 1 ? -1.0f : 0.0f),
+                             P_ == 2 ? 1.0f : (P_ == 3 ? -1.0f : 0.0f), h.M, nsx, nsy);
+          }
+          rnb[j] = mk2(v[0], v[1]);
+        }
+      } else {
+        const Pair<T> SX = splat2(nsx), SY = splat2(nsy);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+          const Pair<T> bs = bshift2(rax[j], ray[j], rbo[j], SX, SY, pk);
+          // (padding slots hold b = +INF: keep their b' at +INF)
+          rnb[j] = mk2(lo2(rbo[j]) < INFINITY ? -lo2(bs) : -INFINITY,
+                       hi2(rbo[j]) < INFINITY ? -hi2(bs) : -INFINITY);
+        }
+      }
+      F = fx_frame(C, nsx, nsy);
+      shifted = true;
+    };
     uint8_t st = bad ? 255 : 0;
     uint32_t pos0 = h.cx < 0.0f ? 1u : 0u, pos1 = h.cy < 0.0f ? 3u : 2u;  // box corner's edges
     double xp = h.cx < 0.0f ? -(double)h.M : (double)h.M;  // serial.hpp:56-58
@@ -564,13 +689,10 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
             uint32_t o0 = tail_idx(c, lim), o1 = tail_idx(c + 1, lim);
 #pragma unroll 1
             for (; c < cend; c += 2) {
-              const T x0 = sax[o0], y0 = say[o0];
-              const T x1 = sax[o1], y1 = say[o1];
-              Pair<T> bp = mk2(sb[o0], sb[o1]);  // original b; b' in the frame:
+              const T x0 = sax[o0], y0 = say[o0], b0 = sb[o0];
+              const T x1 = sax[o1], y1 = say[o1], b1 = sb[o1];
               o0 = tail_idx(c + 2, lim);
               o1 = tail_idx(c + 3, lim);
-              if (shifted) bp = bshift2(mk2(x0, x1), mk2(y0, y1), bp, SXp, SYp, pk);
-              const T b0 = lo2(bp), b1 = hi2(bp);
               const Pair<T> e = fma2(mk2(x0, x1), PX, fma2(mk2(y0, y1), PY, mk2(-b0, -b1)));
               const uint32_t v0 = __ballot_sync(kFull, lo2(e) >= nT && 32 * c + lane < mpos) & t0;
               const uint32_t v1 =
@@ -612,6 +734,26 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
           if (stale) fx_count(p, kFxLazy, lane);
           const bool v = fx_exact_violates<P>(p, h.off, h.M, pi, pos0, pos1, stale, xp, yp);
           stale = false;
+          if (T_ > 16.0f * Sk) {
+            // the band is wide (the optimum is far from the frame): move the
+            // frame onto the exact optimum so the next tests are sharp
+            reshift((float)xp, (float)yp);
+            ppx = (float)(xp - (double)F.sx);
+            ppy = (float)(yp - (double)F.sy);
+            epp = kU32 * fmaxf(fabsf(ppx), fabsf(ppy)) +
+                  2.0f * kU64 * (float)fmax(fabs(xp), fabs(yp)) + 0x1p-120f;
+            // the candidate's b' in the new frame (the event below uses it)
+            if constexpr (L::kLateTma) {
+              hnb = -sb[min((uint32_t)sperm[pi - 4], cap - 1u)];
+            } else {
+              const int sl = (int)(pi >> 5);
+              float vb = 0.0f;
+#pragma unroll
+              for (int j = 0; j < NP; ++j)
+                vb = sl == 2 * j ? lo2(rbo[j]) : (sl == 2 * j + 1 ? hi2(rbo[j]) : vb);
+              hnb = -bshift(hx, hy, __shfl_sync(kFull, vb, f), F.sx, F.sy);
+            }
+          }
           if (!v) continue;
         }
       }
@@ -636,31 +778,29 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
         const float scl = hbp * rl2;
         const float wx = hx * scl, wy = hy * scl;
         const float Wm = fmaxf(fabsf(wx), fabsf(wy));
-        const float Kn = fmaf(C.A, fmaf(1.25f * (30.0f * kU32 + 16.5f * kU64), Wm,
+        const float kn = fmaf(C.A, fmaf(1.25f * (30.0f * kU32 + 16.5f * kU64), Wm,
                                         fmaf(1.25f * 23.0f * kU64, Obig, F.kE * rs)),
-                              F.Kn);
+                              F.Kn) * (1.0f + 0x1p-10f);
+        const float ka = C.Ka * (1.0f + 0x1p-10f);
         FxAcc acc;
         fx_acc_init(acc);
         const Pair<T> WX = splat2(wx), WY = splat2(wy);
-        fx_fold_pairs<0, NP>(rax, ray, rnb, NDX, NDY, WX, WY, s, rel, acc, pk);
+        fx_fold_pairs<0, NP>(rax, ray, rnb, NDX, NDY, WX, WY, kn, ka, s, rel, acc, pk);
         if constexpr (NT > 0) {
           const uint32_t lim = (uint32_t)(mj - 1);
           uint32_t o0 = tail_idx(NS, lim), o1 = tail_idx(NS + 1, lim);
 #pragma unroll 1
           for (int c = NS; c <= s; c += 2) {
-            const T x0 = sax[o0], y0 = say[o0];
-            const T x1 = sax[o1], y1 = say[o1];
-            Pair<T> bp = mk2(sb[o0], sb[o1]);
+            const T x0 = sax[o0], y0 = say[o0], b0 = sb[o0];
+            const T x1 = sax[o1], y1 = say[o1], b1 = sb[o1];
             o0 = tail_idx(c + 2, lim);
             o1 = tail_idx(c + 3, lim);
-            const Pair<T> X = mk2(x0, x1), Y = mk2(y0, y1);
-            if (shifted) bp = bshift2(X, Y, bp, SXp, SYp, pk);
-            const Pair<T> NB = sub2(konst2(pk.nz), bp);
+            const Pair<T> X = mk2(x0, x1), Y = mk2(y0, y1), NB = mk2(-b0, -b1);
             if (c + 1 < s)
-              fx_fold2<false>(X, Y, NB, NDX, NDY, WX, WY, (uint32_t)c, (uint32_t)c + 1, true, true,
-                              acc, pk);
+              fx_fold2<false>(X, Y, NB, NDX, NDY, WX, WY, kn, ka, (uint32_t)c, (uint32_t)c + 1, true,
+                              true, acc, pk);
             else
-              fx_fold2<true>(X, Y, NB, NDX, NDY, WX, WY, (uint32_t)c, (uint32_t)c + 1,
+              fx_fold2<true>(X, Y, NB, NDX, NDY, WX, WY, kn, ka, (uint32_t)c, (uint32_t)c + 1,
                              32 * c < rel, 32 * (c + 1) < rel, acc, pk);
           }
         }
@@ -668,31 +808,30 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
         const float G1 = warp_max_f(acc.h1);
         const uint32_t hold = __ballot_sync(kFull, acc.h1 == G1);
         const int hl = __ffs(hold) - 1;
+        const int src = hl < 0 ? 0 : hl;
         const float G2 = warp_max_f(lane == hl ? acc.h2 : acc.h1);
-        const float R = warp_min_f(acc.r1);
+        const float RL = warp_min_f(acc.rl);
         const float MAL = warp_min_f(acc.mal);
-        const uint32_t oslot = __shfl_sync(kFull, acc.own, hl < 0 ? 0 : hl);
-        const float oal = __shfl_sync(kFull, acc.oal, hl < 0 ? 0 : hl);  // > 0 on the chosen side
-        const float iM = rcp_approx(MAL) * (1.0f + 0x1p-18f);
-        const float aG1 = fabsf(G1);
-        // the top unit's own bound (its |a.d| >= MAL)
-        const float E1 = fmaf(C.Ka, aG1, Kn) * rcp_approx(fmaxf(oal, MAL)) * (1.0f + 0x1p-18f);
-        const float E2 = fmaf(C.Ka, fabsf(G2), Kn) * iM;
-        const float ER = fmaf(C.Ka, fabsf(R), Kn) * iM;
-        const bool cert = (MAL > C.Tpar) && __popc(hold) == 1 && aG1 < INFINITY &&
-                          oslot != kNone &&
-                          (!(G2 > -INFINITY) ||
-                           (G1 - G2 > (E1 + E2) * 1.001f + 4.0f * kU32 * (aG1 + fabsf(G2)))) &&
-                          (!(R < INFINITY) ||
-                           (R - G1 > (E1 + ER) * 1.001f + 4.0f * kU32 * (aG1 + fabsf(R))));
+        const uint32_t oslot = __shfl_sync(kFull, acc.own, src);
+        const float L1 = __shfl_sync(kFull, acc.l1, src);
+        // the winner's lo beats every other unit's hi (unique owner, the
+        // reference's argmax) and the chosen side's hi is below the other
+        // side's lo (non-empty interval); 4u margins cover hi/lo rounding
+        const bool cert = (MAL > C.Tpar) && __popc(hold) == 1 && oslot != kNone &&
+                          fabsf(G1) < INFINITY && fabsf(L1) < INFINITY &&
+                          (L1 > G2 + 4.0f * kU32 * (fabsf(L1) + fabsf(G2))) &&
+                          (G1 + 4.0f * kU32 * (fabsf(G1) + fabsf(RL)) <= RL);
+        const float q1 = 0.5f * (G1 + L1);          // the winner's quotient
+        const float aG1 = fabsf(q1);
         if (cert) {
           // the reference's event resolves to the owner at (oslot, hl): the
           // optimum is that pair's intersection, exactly known, computed lazily
+          const float E1 = 0.505f * (G1 - L1);
           pos0 = pi;
           pos1 = 32u * oslot + (uint32_t)hl;
           stale = true;
-          ppx = fmaf(G1, fdx, wx);
-          ppy = fmaf(G1, fdy, wy);
+          ppx = fmaf(q1, fdx, wx);
+          ppy = fmaf(q1, fdy, wy);
           epp = fmaf(1.1f, E1,
                      fmaf(1.1f * (kRho + 6.0f * kU32 + 2.0f * kU64), aG1,
                           fmaf(1.1f * (11.0f * kU32 + 7.5f * kU64), Wm,
@@ -700,39 +839,14 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
           done = true;
           break;
         }
-        if (pass > 0 || !(aG1 < INFINITY) || hl < 0) break;
+        if (pass > 0 || !(aG1 < INFINITY) || hl < 0 || !(fabsf(L1) < INFINITY)) break;
         // reshift the frame to the candidate point and refold once
-        fx_count(p, kFxReshift, lane);
-        const float nsx = F.sx + fmaf(G1, fdx, wx), nsy = F.sy + fmaf(G1, fdy, wy);
+        const float nsx = F.sx + fmaf(q1, fdx, wx), nsy = F.sy + fmaf(q1, fdy, wy);
+        reshift(nsx, nsy);
+        // the violated constraint's b' in the new frame
         if constexpr (L::kLateTma) {
-          // register chunks: b' from the original b (staging buffer, never
-          // rewritten); the tail computes its b' on the fly (shifted)
-          const Pair<T> SX = splat2(nsx), SY = splat2(nsy);
-#pragma unroll
-          for (int j = 0; j < NP; ++j) {
-            T v[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int K = 2 * j + e;
-              const int P_ = 32 * K + lane;
-              const bool valid = K < NS && (K < L::kAlwaysValid || P_ < mpos);
-              const uint32_t o = min((uint32_t)sperm[K == 0 ? max(P_ - 4, 0) : P_ - 4], cap - 1u);
-              v[e] = (K == 0 && P_ < 4) ? h.M : (valid ? sb[o] : INFINITY);
-            }
-            const Pair<T> bs = bshift2(rax[j], ray[j], mk2(v[0], v[1]), SX, SY, pk);
-            rnb[j] = mk2(v[0] < INFINITY ? -lo2(bs) : -INFINITY, v[1] < INFINITY ? -hi2(bs) : -INFINITY);
-          }
-          hbp = bshift(hx, hy, pi < 4 ? h.M : sb[min((uint32_t)sperm[pi - 4], cap - 1u)], nsx, nsy);
+          hbp = sb[min((uint32_t)sperm[pi - 4], cap - 1u)];
         } else {
-          const Pair<T> SX = splat2(nsx), SY = splat2(nsy);
-#pragma unroll
-          for (int j = 0; j < NP; ++j) {
-            const Pair<T> bs = bshift2(rax[j], ray[j], rbo[j], SX, SY, pk);
-            // (padding slots hold b = +INF: keep their b' at +INF)
-            rnb[j] = mk2(lo2(rbo[j]) < INFINITY ? -lo2(bs) : -INFINITY,
-                         hi2(rbo[j]) < INFINITY ? -hi2(bs) : -INFINITY);
-          }
-          // the violated constraint's original b: its lane's register
           const int sl = (int)(pi >> 5);
           float vb = 0.0f;
 #pragma unroll
@@ -740,15 +854,13 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
             vb = sl == 2 * j ? lo2(rbo[j]) : (sl == 2 * j + 1 ? hi2(rbo[j]) : vb);
           hbp = bshift(hx, hy, __shfl_sync(kFull, vb, f), nsx, nsy);
         }
-        F = fx_frame(C, nsx, nsy);
-        shifted = true;
-        SXp = splat2(nsx);
-        SYp = splat2(nsy);
       }
       if (!done) {
         // the reference's double operations for this event
         fx_count(p, kFxExact, lane);
-        const int r = fx_exact_event<P>(p, h.lp, h.off, mj, pi, h.cx, h.cy, h.M, pos0, pos1, xp, yp);
+        const int r = fx_exact_event<P>(p, h.lp, h.off, mj, pi, h.cx, h.cy, h.M, pos0, pos1, xp, yp,
+                                        L::kLateTma ? sperm : nullptr, L::kLateTma ? sax : nullptr,
+                                        L::kLateTma ? say : nullptr);
         stale = false;
         if (r == 1) {
           st = 1;
@@ -758,6 +870,7 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
           need_exact_lp = true;  // non-finite optimum: whole-LP reference path
           break;
         }
+        reshift((float)xp, (float)yp);  // the frame onto the exact optimum
         ppx = (float)(xp - (double)F.sx);
         ppy = (float)(yp - (double)F.sy);
         epp = kU32 * fmaxf(fabsf(ppx), fabsf(ppy)) +
@@ -803,7 +916,7 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
           const uint32_t o = min((uint32_t)sperm[pos - 4], cap - 1u);
           x = sax[o];
           y = say[o];
-          bb = sb[o];
+          bb = shifted ? __ldg(static_cast<const float*>(p.b) + h.off + o) : sb[o];
         } else {
           const int sl = (int)(pos >> 5), ln = (int)(pos & 31);
           float vx = 0.0f, vy = 0.0f, vb = 0.0f;
@@ -859,6 +972,12 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
       static_cast<double*>(p.value)[lp] = feas ? (double)h.cx * xp + (double)h.cy * yp : 0.0;
       if (p.viol) p.viol[lp] = viol;
       if (p.wu) p.wu[lp] = wu32;
+#ifdef LP2D_FX_TIMELINE
+      uint64_t tl1;  // debug: wu = start (ns), pair[2lp] = duration (ns)
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl1));
+      if (p.wu) p.wu[lp] = tl0;
+      if (p.pair) p.pair[2 * lp] = (int32_t)min(tl1 - tl0, (uint64_t)0x7fffffff);
+#endif
     }
     h = hn;
   }
