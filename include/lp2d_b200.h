@@ -36,7 +36,10 @@ enum {
   LP2D_ERR_PERM_LENGTH = -3,    /* batch.hpp:311-316 length mismatch        */
   LP2D_ERR_BLOCK_WIDTH = -4,    /* batch.hpp:317-319 zero block width       */
   LP2D_ERR_LAYOUT = -5,         /* offsets not 8-aligned / segment too short */
-  LP2D_ERR_BAD_PERM = -6,       /* a perm entry >= m (reported per LP too)  */
+  LP2D_ERR_BAD_PERM = -6,       /* a perm entry >= m: the C ABI reports it per
+                                   LP (status LP2D_INVALID); the C++ and Python
+                                   front-ends throw std::invalid_argument /
+                                   ValueError on it                          */
   LP2D_ERR_ARG = -7,            /* null pointer / bad enum                  */
   LP2D_ERR_UNSUPPORTED = -8,    /* size class not built                     */
   LP2D_ERR_CUDA = -9,           /* CUDA runtime error (see last_error)      */
@@ -113,6 +116,14 @@ typedef struct lp2d_out {
   int32_t* pair;              /* [2n], optional */
   uint32_t* violation_events; /* optional, serial.hpp:148-151 */
   uint64_t* work_units;       /* optional */
+  /* optional: violations per (block, insertion step), the input of the
+   * reference's lane_stats (batch.hpp:84-120, block semantics of run_block,
+   * :149-294) rebuilt on the host (lane_stats.hpp). Block b holds LPs
+   * [b*W, (b+1)*W) for W = opts->block_width; entry b*(max_m+1) + iter
+   * counts the LPs of block b that violated at 1-based insertion step iter.
+   * ceil(n/W) * (max_m+1) entries, max_m = the batch's largest m; the library
+   * zeroes it. */
+  uint32_t* iter_hist;
 } lp2d_out;
 
 void lp2dgpu_default_opts(lp2d_opts* opts);

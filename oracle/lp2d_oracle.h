@@ -80,6 +80,15 @@ int lp2d_oracle_solve_batch_f(int64_t n, const int64_t* offset,
                               const float* M, double eps_par, double eps_feas,
                               int threads, lp2d_oracle_result* out);
 
+/* Per-(block of W LPs, 1-based insertion step) violation counts, hist[(j /
+ * W) * stride + step] (stride >= max m + 1): the input from which the
+ * reference's lane_stats are rebuilt (the GPU's lp2d_out::iter_hist). */
+int lp2d_oracle_iter_hist_d(int64_t n, const int64_t* offset, const int32_t* m,
+                            const double* ax, const double* ay, const double* b,
+                            const uint32_t* perm, const double* c, const double* M,
+                            double eps_par, double eps_feas, int64_t W, int64_t stride,
+                            uint32_t* hist);
+
 /* oracle.hpp solve_bruteforce (O(m^3), m <= 512). Returns -2 above the cap. */
 int lp2d_oracle_bruteforce(const double* ax, const double* ay, const double* b,
                            int64_t m, double cx, double cy, double M,

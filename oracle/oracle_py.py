@@ -76,6 +76,8 @@ def oracle_lib():
         for suf in ("d", "f"):
             fn = getattr(lib, "lp2d_oracle_solve_batch_" + suf)
             fn.argtypes = [C.c_int64] + [C.c_void_p] * 8 + [C.c_double, C.c_double, C.c_int, C.c_void_p]
+        lib.lp2d_oracle_iter_hist_d.argtypes = [C.c_int64] + [C.c_void_p] * 8 + [C.c_double, C.c_double,
+                                                                                  C.c_int64, C.c_int64, C.c_void_p]
         lib.lp2d_oracle_bruteforce.argtypes = [C.c_void_p] * 3 + [C.c_int64] + [C.c_double] * 5 + [C.c_void_p]
         lib.lp2d_oracle_segmented_extremes.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int,
                                                        C.c_void_p, C.c_void_p]
@@ -117,6 +119,8 @@ def ref_lib():
         lib.ref_uniform.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_int64, C.c_void_p]
         lib.ref_contention_ns.restype = C.c_int64
         lib.ref_contention_ns.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_uint64, C.c_int64]
+        lib.ref_batch_lane_stats.restype = C.c_int
+        lib.ref_batch_lane_stats.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int] + [C.c_void_p] * 3
         lib.ref_fill.restype = C.c_int
         lib.ref_fill.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_double, C.c_double] + [C.c_void_p] * 6
@@ -264,3 +268,58 @@ def ref_solve_batch(packed, threads=0, block_width=512, balanced=True):
     finally:
         ref.ref_batch_free(h)
     return fe, x, y, v, st
+
+
+def iter_hist(packed, W):
+    """Oracle violation histogram per (block of W LPs, insertion step)."""
+    f64 = lambda a: np.ascontiguousarray(a, np.float64)
+    n = packed.n
+    stride = int(np.max(packed.m, initial=0)) + 1
+    hist = np.zeros(((n + W - 1) // W) * stride, np.uint32)
+    perm = np.ascontiguousarray(packed.perm, np.uint32)
+    rc = oracle_lib().lp2d_oracle_iter_hist_d(n, _p(np.ascontiguousarray(packed.offset, np.int64)),
+                                              _p(np.ascontiguousarray(packed.m, np.int32)),
+                                              _p(f64(packed.ax)), _p(f64(packed.ay)), _p(f64(packed.b)),
+                                              _p(perm), _p(f64(packed.c)), _p(f64(packed.M)), 1e-12, 1e-9,
+                                              W, stride, _p(hist))
+    if rc:
+        raise ValueError("iter_hist failed")
+    return hist
+
+
+def ref_lane_stats(packed, W, balanced=True, record=False):
+    """The unmodified reference's lane_stats (lane_wu, [total_wu,
+    violation_events, masked, idle, blocks, n_iter], iteration records)."""
+    ref = ref_lib()
+    f64 = lambda a: np.ascontiguousarray(a, np.float64)
+    ax, ay, b, c, M = (f64(a) for a in (packed.ax, packed.ay, packed.b, packed.c, packed.M))
+    perm = np.ascontiguousarray(packed.perm, np.uint32)
+    off = np.ascontiguousarray(packed.offset, np.int64)
+    mm = np.ascontiguousarray(packed.m, np.int32)
+    n = len(mm)
+    h = ref.ref_batch_create(n, _p(off), _p(mm), _p(ax), _p(ay), _p(b), _p(perm), _p(c), _p(M))
+    nb = (n + W - 1) // W
+    lane_wu = np.zeros(nb * W, np.uint64)
+    st = np.zeros(6, np.uint64)
+    it = np.zeros(6 * nb * (int(mm.max(initial=0)) + 1), np.uint64) if record else None
+    try:
+        if ref.ref_batch_lane_stats(h, W, 1 if balanced else 0, 1 if record else 0, _p(lane_wu), _p(st),
+                                    _p(it)):
+            raise ValueError("ref lane stats failed")
+    finally:
+        ref.ref_batch_free(h)
+    recs = it[:6 * int(st[5])].reshape(-1, 6) if record else None
+    return lane_wu, st, recs
+
+
+def ref_bruteforce(ax, ay, b, c, M, eps_par=1e-12, eps_feas=1e-9):
+    """The unmodified reference's solve_bruteforce (oracle.hpp:38-70, vertex
+    enumeration, m <= 512): (feasible, x, y, value)."""
+    ax = np.ascontiguousarray(ax, np.float64); ay = np.ascontiguousarray(ay, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    fe = np.zeros(1, np.uint8); x = np.zeros(1); y = np.zeros(1); v = np.zeros(1)
+    rc = ref_lib().ref_bruteforce(_p(ax), _p(ay), _p(b), len(ax), float(c[0]), float(c[1]), float(M),
+                                  eps_par, eps_feas, _p(fe), _p(x), _p(y), _p(v))
+    if rc:
+        raise ValueError("ref_bruteforce failed")
+    return bool(fe[0]), float(x[0]), float(y[0]), float(v[0])

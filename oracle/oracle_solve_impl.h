@@ -94,10 +94,25 @@ static inline void FN(box_)(int k, T M, T* ax, T* ay, T* b) {
  * Inputs are one LP in the original constraint order, with the insertion
  * order perm (indices 0..m-1). perm may be NULL for identity order.
  * Returns 0 on success, -1 if perm is not a permutation index set. */
+static int FN(solve_hist_)(const S* cax, const S* cay, const S* cb,
+                           const uint32_t* perm, int64_t m, S cx_s, S cy_s, S M_s,
+                           double eps_par_d, double eps_feas_d,
+                           lp2d_oracle_result* out, uint32_t* hist_row);
+
 int FN(lp2d_oracle_solve_)(const S* cax, const S* cay, const S* cb,
                            const uint32_t* perm, int64_t m, S cx_s, S cy_s, S M_s,
                            double eps_par_d, double eps_feas_d,
                            lp2d_oracle_result* out) {
+  return FN(solve_hist_)(cax, cay, cb, perm, m, cx_s, cy_s, M_s, eps_par_d, eps_feas_d, out,
+                         NULL);
+}
+
+/* The same solve, additionally counting each violation at its 1-based
+ * insertion step into hist_row[step] (lane_stats reconstruction tests). */
+static int FN(solve_hist_)(const S* cax, const S* cay, const S* cb,
+                           const uint32_t* perm, int64_t m, S cx_s, S cy_s, S M_s,
+                           double eps_par_d, double eps_feas_d,
+                           lp2d_oracle_result* out, uint32_t* hist_row) {
   const T eps_par = (T)eps_par_d;
   const T eps_feas = (T)eps_feas_d;
   const T cx = (T)cx_s, cy = (T)cy_s, M = (T)M_s;
@@ -118,6 +133,7 @@ int FN(lp2d_oracle_solve_)(const S* cax, const S* cay, const S* cb,
     if (FN(satisfied_)(hx, hy, hb, px, py, eps_feas)) continue;
     viol += 1;
     wu += (uint64_t)(4 + i);
+    if (hist_row) hist_row[i + 1] += 1;
     const FN(line_) l = FN(boundary_of_)(hx, hy, hb);
     FN(interval_) acc;
     acc.u_left = -(T)INFINITY;
@@ -201,6 +217,24 @@ int FN(lp2d_oracle_solve_)(const S* cax, const S* cay, const S* cb,
   out->y = (double)py;
   /* serial.hpp:187 objective_value(c, x) */
   out->value = (double)(cx * px + cy * py);
+  return 0;
+}
+
+/* Violation histogram per (block of W LPs, insertion step): the input of the
+ * reference's lane_stats (batch.hpp:149-294), see include/lp2d_b200.h. */
+int FN(lp2d_oracle_iter_hist_)(int64_t n, const int64_t* offset, const int32_t* m,
+                               const S* ax, const S* ay, const S* b,
+                               const uint32_t* perm, const S* c, const S* M,
+                               double eps_par, double eps_feas, int64_t W,
+                               int64_t stride, uint32_t* hist) {
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t o = offset[j];
+    lp2d_oracle_result r;
+    const int rc = FN(solve_hist_)(ax + o, ay + o, b + o, perm ? perm + o : NULL, m[j],
+                                   c[2 * j], c[2 * j + 1], M[j], eps_par, eps_feas, &r,
+                                   hist + (j / W) * stride);
+    if (rc) return rc;
+  }
   return 0;
 }
 

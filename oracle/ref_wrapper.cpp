@@ -299,6 +299,42 @@ int64_t ref_batch_solve(void* h, int64_t block_width, int scheduler,
   }
 }
 
+// lane_stats of solve_batch (batch.hpp:94-107): lane_wu (nblocks * width
+// entries) and [total_wu, violation_events, masked_lane_iterations,
+// idle_wu_steps, blocks, iterations recorded]. Returns 0, -1 on error.
+int ref_batch_lane_stats(void* h, int64_t block_width, int scheduler, int record,
+                         uint64_t* lane_wu, uint64_t* stats, uint64_t* iter_wu) {
+  const auto* bt = static_cast<const lp2d::batch*>(h);
+  lp2d::block_config cfg;
+  cfg.block_width = static_cast<std::size_t>(block_width);
+  cfg.scheduler = scheduler == 0 ? lp2d::scheduler_kind::naive : lp2d::scheduler_kind::balanced;
+  cfg.workers = 1;
+  cfg.record_iterations = record != 0;
+  try {
+    const lp2d::batch_result r = lp2d::solve_batch(*bt, cfg, lp2d::tolerance{});
+    std::memcpy(lane_wu, r.stats.lane_wu.data(), sizeof(uint64_t) * r.stats.lane_wu.size());
+    stats[0] = r.stats.total_wu;
+    stats[1] = r.stats.violation_events;
+    stats[2] = r.stats.masked_lane_iterations;
+    stats[3] = r.stats.idle_wu_steps;
+    stats[4] = r.stats.blocks;
+    stats[5] = r.stats.iterations.size();
+    if (iter_wu)
+      for (std::size_t k = 0; k < r.stats.iterations.size(); ++k) {
+        const auto& it = r.stats.iterations[k];
+        iter_wu[6 * k + 0] = it.block;
+        iter_wu[6 * k + 1] = it.iteration;
+        iter_wu[6 * k + 2] = it.active_lanes;
+        iter_wu[6 * k + 3] = it.masked_lanes;
+        iter_wu[6 * k + 4] = it.wu_count;
+        iter_wu[6 * k + 5] = it.idle_steps;
+      }
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
 // Serial solve of every LP across `threads` std::threads.
 int64_t ref_batch_solve_serial_threads(void* h, unsigned threads,
                                        double eps_par, double eps_feas,

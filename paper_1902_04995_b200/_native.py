@@ -75,6 +75,7 @@ class Out(C.Structure):
         ("pair", C.c_void_p),
         ("violation_events", C.c_void_p),
         ("work_units", C.c_void_p),
+        ("iter_hist", C.c_void_p),
     ]
 
 

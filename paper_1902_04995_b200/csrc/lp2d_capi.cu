@@ -79,7 +79,11 @@ struct DeviceGuard {
 };
 
 int ensure_device(int dev) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || dev < 0 || dev >= ndev || dev >= 64)
+    return fail(LP2D_ERR_ARG, "bad device ordinal " + std::to_string(dev));
   DeviceState& d = g_dev[dev];
+  std::lock_guard<std::mutex> lock(d.mu);
   if (d.init) return 0;
   CUDA_TRY(cudaSetDevice(dev));
   CUDA_TRY(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, dev));
@@ -108,6 +112,10 @@ uint32_t* take_counter(int dev) {
 
 // Register slot classes: NS slots hold m + 4 positions (box included).
 constexpr int kSlotClasses[] = {1, 2, 4, 5, 6, 9, 10, 18, 33, 65, 129};
+constexpr int kNumSlotClasses = (int)(sizeof(kSlotClasses) / sizeof(kSlotClasses[0]));
+static_assert(kNumSlotClasses <= kMaxSlotClasses, "BinSpec::slots holds every register class");
+static_assert(kNumSlotClasses + 1 <= 16, "host_counts holds every class + the large class");
+static_assert(kLaneMaxM + 1 + kNumSlotClasses + 64 <= kMaxBins, "bins fit kMaxBins");
 
 template <typename T>
 constexpr int max_nslot() {
@@ -135,6 +143,8 @@ int launch_late_tma_cap(KParams kp, int dev, cudaStream_t stream) {
     int warps = 0, blocks = 0;
   };
   static Shape shape[64];
+  static std::mutex mu;  // host threads of a multi-GPU solve initialise concurrently
+  std::unique_lock<std::mutex> lock(mu);
   if (!shape[dev].warps) {
     int optin = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -150,6 +160,7 @@ int launch_late_tma_cap(KParams kp, int dev, cudaStream_t stream) {
     shape[dev] = best;
   }
   const Shape sh = shape[dev];
+  lock.unlock();
   const size_t smem = (size_t)sh.warps * (L::kBuf + 8);
   const int64_t want = (kp.n_list + sh.warps - 1) / sh.warps;
   const int64_t maxb = (int64_t)sh.blocks * g_dev[dev].sm_count;
@@ -177,6 +188,8 @@ int launch_warp_kernel(KParams kp, int dev, cudaStream_t stream, int64_t max_m =
   constexpr int kWarpsPerCta = L::kWarps;
   auto kern = k_solve_warp<T, P, NS, NT>;
   static int blocks_per_sm[64] = {0};
+  static std::mutex mu;  // concurrent first use from multi-GPU host threads
+  std::lock_guard<std::mutex> lock(mu);
   // (experiment knob: LP2D_B200_SMEM_PAD bytes of extra shared memory per CTA
   // lower the resident warps, for occupancy-sensitivity measurements)
   static const size_t pad = [] {
@@ -219,6 +232,8 @@ int launch_lane_kernel(KParams kp, int dev, cudaStream_t stream) {
   auto kern = k_solve_lanes<T, P, MAXM>;
   constexpr size_t smem = LaneTile<T, MAXM>::kSmem;
   static int blocks_per_sm[64] = {0};
+  static std::mutex mu;  // concurrent first use from multi-GPU host threads
+  std::lock_guard<std::mutex> lock(mu);
   if (!blocks_per_sm[dev]) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int b = 0;
@@ -259,6 +274,8 @@ template <typename T, typename P>
 int launch_global_kernel(KParams kp, int dev, cudaStream_t stream) {
   auto kern = k_solve_global<T, P>;
   static int blocks_per_sm[64] = {0};
+  static std::mutex mu;  // concurrent first use from multi-GPU host threads
+  std::lock_guard<std::mutex> lock(mu);
   if (!blocks_per_sm[dev]) {
     int b = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kWarpsPerCta * 32, 0));
@@ -762,7 +779,12 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   size_t off_pair = off_v + al(sizeof(T) * cnt);
   size_t off_viol = off_pair + al(sizeof(int32_t) * 2 * cnt);
   size_t off_wu = off_viol + al(sizeof(uint32_t) * cnt);
-  size_t total = off_wu + al(sizeof(uint64_t) * cnt);
+  // (lane_stats histogram: the rows of the blocks this shard touches)
+  const int64_t W = o->block_width;
+  const int64_t row0 = lo / W, rows = out->iter_hist ? (hi - 1) / W - row0 + 1 : 0;
+  const int64_t hstride = max_m + 1;
+  size_t off_hist = off_wu + al(sizeof(uint64_t) * cnt);
+  size_t total = off_hist + al(sizeof(uint32_t) * rows * hstride);
   if (d.arena_bytes < total) {
     if (d.arena) CUDA_TRY(cudaFree(d.arena));
     d.arena = nullptr;
@@ -807,8 +829,19 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   kp.pair = reinterpret_cast<int32_t*>(A + off_pair);
   kp.viol = reinterpret_cast<uint32_t*>(A + off_viol);
   kp.wu = reinterpret_cast<uint64_t*>(A + off_wu);
+  if (rows) {
+    kp.iter_hist = reinterpret_cast<uint32_t*>(A + off_hist);
+    kp.hist_lp0 = lo - row0 * W;  // local LP 0 sits at this offset within row 0
+    kp.hist_w = (int32_t)W;
+    kp.hist_stride = (int32_t)hstride;
+    CUDA_TRY(cudaMemsetAsync(kp.iter_hist, 0, sizeof(uint32_t) * rows * hstride, s));
+  }
   if (int rc = solve_device_batch<S>(kp, E, min_m, max_m, b->perm_bits, o->scheduler, dev, s, true))
     return rc;
+  std::vector<uint32_t> hist((size_t)(rows * hstride));
+  if (rows)
+    CUDA_TRY(cudaMemcpyAsync(hist.data(), kp.iter_hist, sizeof(uint32_t) * rows * hstride,
+                             cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(out->status + lo, A + off_st, cnt, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(static_cast<T*>(out->x) + lo, A + off_x, sizeof(T) * cnt,
                            cudaMemcpyDeviceToHost, s));
@@ -826,6 +859,12 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     CUDA_TRY(cudaMemcpyAsync(out->work_units + lo, A + off_wu, sizeof(uint64_t) * cnt,
                              cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
+  if (rows) {
+    // shards may share a block row: accumulate (the caller's buffer was zeroed)
+    static std::mutex hist_mu;
+    std::lock_guard<std::mutex> lock(hist_mu);
+    for (int64_t q = 0; q < rows * hstride; ++q) out->iter_hist[row0 * hstride + q] += hist[q];
+  }
   return 0;
 }
 
@@ -861,6 +900,16 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
     kp.pair = out->pair;
     kp.viol = out->violation_events;
     kp.wu = out->work_units;
+    if (out->iter_hist) {
+      const int64_t W = o->block_width;
+      const int64_t rows = (b->n + W - 1) / W;
+      CUDA_TRY(cudaMemsetAsync(out->iter_hist, 0, sizeof(uint32_t) * rows * (b->max_m + 1),
+                               static_cast<cudaStream_t>(o->stream)));
+      kp.iter_hist = out->iter_hist;
+      kp.hist_lp0 = 0;
+      kp.hist_w = (int32_t)W;
+      kp.hist_stride = (int32_t)(b->max_m + 1);
+    }
     int64_t E = 0;  // scalar elements (offset[n]), needed to widen fp32 storage
     if constexpr (sizeof(S) == 4) {
       CUDA_TRY(cudaMemcpy(&E, b->offset + b->n, sizeof(int64_t), cudaMemcpyDeviceToHost));
@@ -882,6 +931,9 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
   }
   if (b->perm_bits == 16 && max_m > 65536)
     return fail(LP2D_ERR_ARG, "u16 permutations need m <= 65536");
+  if (out->iter_hist)
+    std::memset(out->iter_hist, 0,
+                sizeof(uint32_t) * ((b->n + o->block_width - 1) / o->block_width) * (max_m + 1));
   int use = o->n_gpus > 0 ? std::min(o->n_gpus, ndev) : ndev;
   use = (int)std::min<int64_t>(std::min(use, 64), b->n);
   std::vector<int64_t> cut(use + 1, 0);

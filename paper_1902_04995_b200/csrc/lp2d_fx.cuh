@@ -760,6 +760,7 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
       // ---- event at position pi: 1D LP over positions [0, pi) ----------------
       viol += 1;
       wu32 += pi;  // considered.size() (serial.hpp:176-179)
+      if (lane == 0) note_event(p, h.lp, pi);
       const float len2 = fmaf(hx, hx, hy * hy);
       const bool line_ok = (len2 >= 0x1p-100f) & (len2 <= 0x1p100f);
       const float rs = rsqrt_approx(len2), rl2 = rcp_approx(len2);
@@ -889,7 +890,7 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
       h64.cy = h.cy;
       h64.M = h.M;
       LPState<double> S64;
-      solve_exact_global<double, P, float>(p, h64, p.eps_par, p.eps_feas, p.eps_hi, S64);
+      solve_exact_global<double, P, float>(p, h64, p.eps_par, p.eps_feas, p.eps_hi, S64, viol);
       st = S64.st;
       pos0 = S64.pos0;
       pos1 = S64.pos1;

@@ -69,7 +69,19 @@ struct KParams {
   // K4 certificate factors (host-computed from the tolerance, lp2d_fx.cuh):
   // Ka = A*fx_ka, Tpar = A*fx_tp, Ec = (|cx|+|cy|)*fx_ec, eps_feas rounded up
   float fx_ka, fx_tp, fx_ec, fx_eps;
+  // Optional per-(block, insertion step) violation histogram (lane_stats with
+  // the reference's block semantics, batch.hpp:149-294, are rebuilt from it on
+  // the host): iter_hist[((hist_lp0 + lp) / hist_w) * hist_stride + iter] +=
+  // 1 per violation at insertion step iter = pi - 3 (1-based).
+  uint32_t* iter_hist;
+  int64_t hist_lp0;
+  int32_t hist_w, hist_stride;
 };
+
+__device__ __forceinline__ void note_event(const KParams& p, int64_t lp, uint32_t pi) {
+  if (p.iter_hist)
+    atomicAdd(p.iter_hist + ((p.hist_lp0 + lp) / p.hist_w) * (int64_t)p.hist_stride + (pi - 3), 1u);
+}
 
 template <typename T>
 struct Eps {
@@ -520,9 +532,11 @@ __device__ __forceinline__ bool resolve_event(LPState<T>& S, const Acc<T>& acc,
 // magnitudes leave the fast path's proven range (non-finite or huge
 // coefficients, a non-finite running optimum); rare, so simple.
 template <typename T, typename P, typename SS = T>
+// skip_note: events already noted by a partial fast solve of this LP (the
+// exact re-solve repeats them; note_event records each event once).
 __device__ __noinline__ void solve_exact_global(const KParams& p, const Header<T>& h,
                                                 T eps_par, T eps_feas, T eps_hi,
-                                                LPState<T>& S) {
+                                                LPState<T>& S, uint32_t skip_note = 0) {
   const int lane = threadIdx.x & 31;
   const SS* ax = static_cast<const SS*>(p.ax) + h.off;
   const SS* ay = static_cast<const SS*>(p.ay) + h.off;
@@ -549,6 +563,7 @@ __device__ __noinline__ void solve_exact_global(const KParams& p, const Header<T
     const uint32_t pi = 4u + (uint32_t)iv;
     S.viol += 1;
     S.wu += pi;
+    if (lane == 0 && S.viol > skip_note) note_event(p, h.lp, pi);
     const Line<T> l = boundary_of((T)ax[o], (T)ay[o], (T)b[o]);
     const Acc<T> acc = fold_exact_global<T, P, SS>(p, h.off, pi, l, h.M, eps_par, eps_feas, eps_hi);
     if (!resolve_event(S, acc, l, pi, h, cthr, eps_feas)) return;
@@ -600,6 +615,7 @@ __global__ void __launch_bounds__(128) k_solve_naive(const __grid_constant__ KPa
     if (satisfied(hx, hy, hb, px, py, eps_feas)) continue;
     viol += 1;
     wu += 4 + (uint32_t)i;
+    note_event(p, h.lp, 4u + (uint32_t)i);
     const Line<T> l = boundary_of(hx, hy, hb);
     Acc<T> acc;
     acc.uL = -T(INFINITY);
@@ -813,6 +829,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
       if (v) {
         S.viol += 1;
         S.wu += (uint32_t)i;
+        note_event(p, h.lp, (uint32_t)i);
         l = boundary_of(sx[at(i, lane)], sy[at(i, lane)], sb[at(i, lane)]);
       }
       const int nv = __popc(vm);
@@ -1121,6 +1138,7 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
       // ---- event at position pi ------------------------------------------
       S.viol += 1;
       S.wu += (uint32_t)pi;
+      if (tid == 0) note_event(p, h.lp, (uint32_t)pi);
       T hx, hy, hb;
       pos(pi, h.M, hx, hy, hb);
       const Line<T> l = boundary_fast(hx, hy, hb);
@@ -1194,7 +1212,7 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
       start = pi + 1;
     }
     if (need_exact) {
-      if (wid == 0) solve_exact_global<T, P>(p, h, eps_par, eps_feas, eps_hi, S);
+      if (wid == 0) solve_exact_global<T, P>(p, h, eps_par, eps_feas, eps_hi, S, S.viol);
     }
     if (tid == 0) {
       uint8_t st = S.st;
@@ -1274,17 +1292,19 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_solve_global(const __grid
 // Branch-free: the class is the number of classes too small for m (slots
 // ascend), counted over a fixed-size unrolled table (no dynamic indexing of
 // the parameter array, no loop-carried branch).
+constexpr int kMaxSlotClasses = 12;  // BinSpec::slots capacity (static_assert in lp2d_capi.cu)
+
 __device__ __forceinline__ int size_class(int32_t m, const int32_t* slots, int nreg) {
   int c = 0;
 #pragma unroll
-  for (int k = 0; k < 12; ++k) c += (k < nreg && m + 4 > 32 * slots[k]) ? 1 : 0;
+  for (int k = 0; k < kMaxSlotClasses; ++k) c += (k < nreg && m + 4 > 32 * slots[k]) ? 1 : 0;
   return c;
 }
 
 constexpr int kMaxBins = 128;
 
 struct BinSpec {
-  int32_t slots[12];
+  int32_t slots[kMaxSlotClasses];
   int32_t nreg;
   int32_t lane_bins;  // > 0: class 0 is split into one bin per m in [0, lane_bins)
   int32_t cta_bins;   // > 1: the large class is split by m, largest first

@@ -129,15 +129,35 @@ class Solution:
 
 
 @dataclass
+class IterationRecord:
+    """batch.hpp:84-92 iteration_record (record_iterations)."""
+
+    block: int = 0
+    iteration: int = 0
+    active_lanes: int = 0
+    masked_lanes: int = 0
+    wu_count: int = 0
+    idle_steps: int = 0
+    lane_wu: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+
+
+@dataclass
 class LaneStats:
-    """batch.hpp:94-107 (GPU meaning: counters are exact per-LP sums; lane_wu
-    is per LP — the 'lane' that owns it — see DESIGN.md)."""
+    """batch.hpp:94-107 with the reference's block semantics: blocks of
+    block_width LPs stepping through insertion steps in lockstep (run_block,
+    batch.hpp:149-294). The GPU solves LPs independently; these counters are
+    rebuilt exactly from the GPU's per-(block, step) violation histogram
+    (lp2d_out::iter_hist, rebuild_lane_stats), so lane_imbalance() means what
+    it means in the reference."""
 
     block_width: int = 0
     blocks: int = 0
     lane_wu: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
     total_wu: int = 0
     violation_events: int = 0
+    masked_lane_iterations: int = 0
+    idle_wu_steps: int = 0
+    iterations: List[IterationRecord] = field(default_factory=list)
 
 
 @dataclass
@@ -348,7 +368,8 @@ def _opts(cfg: BlockConfig, tol: Tolerance, device: int = 0, stream: int = 0) ->
 
 
 def solve_packed(pb: PackedBatch, cfg: BlockConfig = BlockConfig(), tol: Tolerance = Tolerance(),
-                 out: Optional[PackedResult] = None) -> PackedResult:
+                 out: Optional[PackedResult] = None,
+                 iter_hist: Optional[np.ndarray] = None) -> PackedResult:
     """Host-buffer solve through the C ABI (copies in/out inside the call)."""
     if pb.n == 0:
         raise ValueError("solve_batch: empty batch")
@@ -367,7 +388,8 @@ def solve_packed(pb: PackedBatch, cfg: BlockConfig = BlockConfig(), tol: Toleran
                    N.MEM_HOST, c.ctypes.data, M.ctypes.data, 0, 0)
     o = _opts(cfg, tol)
     r = N.Out(out.status.ctypes.data, out.x.ctypes.data, out.y.ctypes.data, out.value.ctypes.data,
-              out.pair.ctypes.data, out.violation_events.ctypes.data, out.work_units.ctypes.data)
+              out.pair.ctypes.data, out.violation_events.ctypes.data, out.work_units.ctypes.data,
+              iter_hist.ctypes.data if iter_hist is not None else None)
     fn = N.lib().lp2dgpu_solve_f32 if dt == np.float32 else N.lib().lp2dgpu_solve_f64
     rc = fn(C.byref(s), C.byref(o), C.byref(r))
     if rc:
@@ -491,7 +513,10 @@ def solve_batch(b: Batch, cfg: BlockConfig = BlockConfig(), tol: Tolerance = Tol
     if cfg.block_width == 0:
         raise ValueError("solve_batch: block width must be positive")
     pb = PackedBatch.from_batch(b, dtype=dtype)
-    r = solve_packed(pb, cfg, tol)
+    W = int(cfg.block_width)
+    nb = (pb.n + W - 1) // W
+    hist = np.zeros(nb * (int(pb.m.max(initial=0)) + 1), np.uint32)
+    r = solve_packed(pb, cfg, tol, iter_hist=hist)
     sols = []
     for j in range(pb.n):
         st = int(r.status[j])
@@ -500,10 +525,89 @@ def solve_batch(b: Batch, cfg: BlockConfig = BlockConfig(), tol: Tolerance = Tol
                              float(r.value[j]) if feas else 0.0, st,
                              (int(r.pair[j, 0]), int(r.pair[j, 1])),
                              int(r.violation_events[j]), int(r.work_units[j])))
-    wu = r.work_units.astype(np.uint64)
-    stats = LaneStats(block_width=cfg.block_width, blocks=(pb.n + 31) // 32, lane_wu=wu,
-                      total_wu=int(wu.sum()), violation_events=int(r.violation_events.sum()))
+    if (r.status == INVALID).any():
+        # a permutation entry >= m: the reference's solve would index out of
+        # range; the front-end refuses instead of returning a value
+        bad = np.nonzero(r.status == INVALID)[0]
+        raise ValueError("solve_batch: permutation entry out of range for LP(s) %s" % bad[:8].tolist())
+    stats = rebuild_lane_stats(pb.m, r.status, r.pair, pb.perm, pb.offset, r.work_units, hist, W,
+                               cfg.scheduler, cfg.record_iterations)
     return BatchResult(sols, stats)
+
+
+def rebuild_lane_stats(m: np.ndarray, status: np.ndarray, pair: np.ndarray,
+                       perm: np.ndarray, offset: np.ndarray, work_units: np.ndarray,
+                       hist: np.ndarray, block_width: int, scheduler: SchedulerKind,
+                       record_iterations: bool = False) -> LaneStats:
+    """The reference's lane_stats (batch.hpp:149-294, 327-371) from a solve's
+    per-LP results and its (block, insertion step) violation histogram:
+    per block, every executed step masks the lanes that are past their m, out
+    of the batch, or infeasible (from the step of their infeasible event,
+    found as the insertion position of the defining pair's violated
+    constraint); the balanced deal gives lane l ceil((active*prefix - l)/W)
+    units (prefix = 3 + step), the naive deal gives each LP's lane its own
+    work units and charges the others prefix idle slots per active step."""
+    W = int(block_width)
+    n = len(m)
+    nb = (n + W - 1) // W
+    stride = len(hist) // max(nb, 1)
+    if hist is None:  # (only the naive lane_wu/total can be rebuilt without it)
+        hist = np.zeros(nb, np.uint32)
+        stride = 1
+    H = np.asarray(hist, np.int64).reshape(nb, stride)
+    m64 = np.asarray(m, np.int64)
+    inf = np.asarray(status) == INFEASIBLE
+    # step of the infeasible event: position of the violated constraint + 1
+    t = np.full(n, np.iinfo(np.int64).max, np.int64)
+    for j in np.nonzero(inf)[0]:
+        o = int(offset[j])
+        pos = np.nonzero(perm[o:o + int(m[j])] == pair[j, 0])[0]
+        t[j] = int(pos[0]) + 1
+    e = np.where(inf, np.minimum(m64, t), m64)  # lane j keeps the block going while step < e_j
+    balanced = SchedulerKind(scheduler) == SchedulerKind.balanced
+    lane_wu = np.zeros(nb * W, np.uint64)
+    st = LaneStats(block_width=W, blocks=nb, lane_wu=lane_wu)
+    for b in range(nb):
+        js = np.arange(b * W, min(n, (b + 1) * W))
+        lp_max = int(m64[js].max(initial=0))
+        last = min(lp_max, max(1, int(e[js].max(initial=0))))
+        if lp_max == 0:
+            continue
+        steps = np.arange(1, last + 1)
+        # masked lanes: !live (W - count), past m, or infeasible before the step
+        past = (steps[None, :] > m64[js][:, None]) | (steps[None, :] > t[js][:, None])
+        masked = (W - len(js)) + past.sum(axis=0)
+        active = H[b, 1:last + 1]
+        prefix = 3 + steps
+        st.masked_lane_iterations += int(masked.sum())
+        st.violation_events += int(active.sum())
+        if balanced:
+            wu = active * prefix
+            q, r = wu // W, wu % W
+            lanes = np.arange(W)
+            per_lane = q.sum() + (lanes[None, :] < r[:, None]).sum(axis=0)
+            lane_wu[b * W:(b + 1) * W] = per_lane.astype(np.uint64)
+            idle = ((wu + W - 1) // W) * W - wu
+        else:
+            lane_wu[b * W:b * W + len(js)] = np.asarray(work_units, np.uint64)[js]
+            idle = np.where(active > 0, prefix * (W - active), 0)
+            wu = active * prefix
+        st.idle_wu_steps += int(idle.sum())
+        if record_iterations:
+            for k, it in enumerate(steps):
+                lw = np.zeros(W, np.uint32)
+                if active[k]:
+                    if balanced:
+                        lw[:] = q[k]
+                        lw[:r[k]] += 1
+                    else:
+                        # lanes of the LPs that violated at this step: not
+                        # recoverable from the histogram alone (counts only)
+                        lw = np.zeros(W, np.uint32)
+                st.iterations.append(IterationRecord(b, int(it), int(active[k]), int(masked[k]),
+                                                     int(wu[k]), int(idle[k]), lw))
+    st.total_wu = int(lane_wu.sum())
+    return st
 
 
 def lane_imbalance(stats: LaneStats) -> float:

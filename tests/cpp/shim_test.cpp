@@ -46,6 +46,29 @@ int main() {
       b.permutations[i] = shuffle(20, 2000 + i);
     }
     const batch_result r = b200::solve_batch(b, {}, tol);
+    // lane_stats with the reference's block semantics, both schedulers and
+    // an odd block width (rebuilt from the GPU's violation histogram)
+    for (auto sched : {scheduler_kind::balanced, scheduler_kind::naive}) {
+      block_config cfg;
+      cfg.scheduler = sched;
+      cfg.block_width = 7;
+      cfg.record_iterations = true;
+      const batch_result g = b200::solve_batch(b, cfg, tol);
+      const batch_result c = solve_batch(b, cfg, tol);
+      CHECK(g.stats.lane_wu == c.stats.lane_wu);
+      CHECK(g.stats.blocks == c.stats.blocks);
+      CHECK(g.stats.masked_lane_iterations == c.stats.masked_lane_iterations);
+      CHECK(g.stats.idle_wu_steps == c.stats.idle_wu_steps);
+      CHECK(g.stats.iterations.size() == c.stats.iterations.size());
+      for (std::size_t k = 0; k < g.stats.iterations.size() && k < c.stats.iterations.size(); ++k) {
+        CHECK(g.stats.iterations[k].active_lanes == c.stats.iterations[k].active_lanes);
+        CHECK(g.stats.iterations[k].masked_lanes == c.stats.iterations[k].masked_lanes);
+        CHECK(g.stats.iterations[k].idle_steps == c.stats.iterations[k].idle_steps);
+        if (sched == scheduler_kind::balanced)
+          CHECK(g.stats.iterations[k].lane_wu == c.stats.iterations[k].lane_wu);
+      }
+      CHECK(lane_imbalance(g.stats) == lane_imbalance(c.stats));
+    }
     std::size_t infeasible = 0;
     for (std::size_t i = 0; i < b.problems.size(); ++i) {
       const solution s = solve(b.problems[i], b.permutations[i], tol);
@@ -73,7 +96,10 @@ int main() {
     block_config zero;
     zero.block_width = 0;
     try { b200::solve_batch(replicate(gen({10, 1}), 2, 1), zero); } catch (const std::invalid_argument&) { ++thrown; }
-    CHECK(thrown == 4);
+    batch d = replicate(gen({10, 1}), 2, 1);  // permutation entry out of range
+    d.permutations[1].order[3] = 99;
+    try { b200::solve_batch(d); } catch (const std::invalid_argument&) { ++thrown; }
+    CHECK(thrown == 5);
   }
   std::printf(failures ? "shim_test: %d failures\n" : "shim_test: ok%d\n", failures);
   return failures ? 1 : 0;
