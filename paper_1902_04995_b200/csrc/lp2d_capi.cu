@@ -449,8 +449,80 @@ bool fx_class(int cls) {
   return on && cls >= 1 && cls < n_reg_classes<double>();
 }
 
+// ---- fp32 storage: K5 (k_solve_fs, lp2d_fs.cuh) ---------------------------
+// Run-time CTA shape: the most resident warps for the buffer size, at most
+// REGW warps per CTA (the kernel's register budget).
+template <typename P, int CAP, int NBUF, int REGW>
+int launch_fs(KParams kp, int dev, cudaStream_t stream) {
+  using L = FsLayout<P, CAP>;
+  auto kern = k_solve_fs<P, CAP, NBUF, REGW>;
+  constexpr size_t per_warp = (size_t)NBUF * (L::kBuf + 8);
+  struct Shape {
+    int warps = 0, blocks = 0;
+  };
+  static Shape shape[64];
+  static std::mutex mu;
+  Shape sh;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!shape[dev].warps) {
+      int optin = 0;
+      CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+      Shape best;
+      for (int w = 1; w <= std::min(REGW, 32) && (size_t)w * per_warp <= (size_t)optin; ++w) {
+        int b = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, w * 32, (size_t)w * per_warp));
+        if (b * w > best.blocks * best.warps) best = Shape{w, b};
+      }
+      if (best.blocks < 1) return fail(LP2D_ERR_CUDA, "fs kernel does not fit on an SM");
+      shape[dev] = best;
+    }
+    sh = shape[dev];
+  }
+  const size_t smem = (size_t)sh.warps * per_warp;
+  const int64_t want = (kp.n_list + sh.warps - 1) / sh.warps;
+  const int64_t maxb = (int64_t)sh.blocks * g_dev[dev].sm_count;
+  const int grid = (int)std::max<int64_t>(1, std::min(want, maxb));
+  kp.total_warps = grid * sh.warps;
+  kp.counter = take_counter(dev);
+  kern<<<grid, sh.warps * 32, smem, stream>>>(kp);
+  note_launch();
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// 0: K4 only, 1: K5 for the classes where it is faster (default), 2: K5 for all.
+int fs_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("LP2D_B200_FS");
+    if (!e) return 1;
+    if (e[0] == '0') return 0;
+    return std::strcmp(e, "all") == 0 ? 2 : 1;
+  }();
+  return mode;
+}
+
 template <typename P>
 int launch_fx_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t max_m) {
+  // K5 where it measured faster than K4 (B200, per uniform batch; DESIGN.md
+  // §3): the 317 <= m <= 572 class (m = 500: 343 vs 439 us per 2^15 LPs).
+  // Below, K4's register-resident chunks win (m = 128: 664 vs 876 us per
+  // 2^17); at m = 1024 the two tie (277 vs 283 us per 2^14).
+  // LP2D_B200_FS=all routes every class <= 1052 to K5, =0 none (A/B knobs).
+  const int fs = fs_mode();
+  if (fs == 2 || (fs == 1 && kSlotClasses[cls] == 18)) {
+    switch (kSlotClasses[cls]) {
+      case 2: return launch_fs<P, 60, 2, 20>(kp, dev, s);
+      case 4: return launch_fs<P, 124, 2, 20>(kp, dev, s);
+      case 5: return launch_fs<P, 156, 2, 20>(kp, dev, s);
+      case 6: return launch_fs<P, 188, 2, 20>(kp, dev, s);
+      case 9: return launch_fs<P, 284, 2, 20>(kp, dev, s);
+      case 10: return launch_fs<P, 316, 2, 20>(kp, dev, s);
+      case 18: return launch_fs<P, 572, 1, 20>(kp, dev, s);
+      case 33: return launch_fs<P, 1052, 1, 15>(kp, dev, s);
+    }
+  }
   switch (kSlotClasses[cls]) {
     case 2: return launch_fx<P, 2, 0>(kp, max_m, dev, s);
     case 4: return launch_fx<P, 4, 0>(kp, max_m, dev, s);

@@ -1,0 +1,20 @@
+"""Every fp32-storage kernel variant (K4 register/tail classes, K5
+insertion-order classes; the library picks per size class, the A/B knob
+LP2D_B200_FS forces either) is bit-identical to the reference on the same
+inputs. Each variant runs in its own process (the knob is read once)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("mode", ["0", "all"])
+def test_fp32_kernel_variant_parity(mode):
+    env = dict(os.environ, LP2D_B200_FS=mode)
+    r = subprocess.run([sys.executable, os.path.join(HERE, "variant_check.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
