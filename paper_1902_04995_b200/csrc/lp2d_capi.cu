@@ -227,9 +227,9 @@ bool tiny_uses_lanes() {
   return lanes;
 }
 
-template <typename T, typename P, int MAXM = kLaneMaxM>
+template <typename T, typename P, int MAXM = kLaneMaxM, typename S = T>
 int launch_lane_kernel(KParams kp, int dev, cudaStream_t stream) {
-  auto kern = k_solve_lanes<T, P, MAXM>;
+  auto kern = k_solve_lanes<T, P, MAXM, S>;
   constexpr size_t smem = LaneTile<T, MAXM>::kSmem;
   static int blocks_per_sm[64] = {0};
   static std::mutex mu;  // concurrent first use from multi-GPU host threads
@@ -296,9 +296,9 @@ int launch_global_kernel(KParams kp, int dev, cudaStream_t stream) {
 // (k_solve_cta). Capacity = the class's largest LP, bounded by the opt-in
 // shared memory per block; bigger LPs are solved by the CTA's warp 0 from
 // global memory. 512 threads when one CTA fills the SM, else 256.
-template <typename T, typename P, int THREADS>
+template <typename T, typename P, int THREADS, typename S = T>
 int launch_cta_t(KParams kp, int64_t cap, size_t smem, int dev, cudaStream_t stream) {
-  auto kern = k_solve_cta<T, P, THREADS>;
+  auto kern = k_solve_cta<T, P, THREADS, S>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int b = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, THREADS, smem));
@@ -313,19 +313,19 @@ int launch_cta_t(KParams kp, int64_t cap, size_t smem, int dev, cudaStream_t str
   return 0;
 }
 
-template <typename T, typename P>
+template <typename T, typename P, typename S = T>
 int launch_cta_kernel(KParams kp, int64_t max_m, int dev, cudaStream_t stream) {
   int optin = 0, per_sm = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   CUDA_TRY(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
   int64_t cap = std::max<int64_t>(16, ((max_m + 15) / 16) * 16);
-  while (cap > 16 && CtaBuffers<T, P>::bytes(cap) > (size_t)optin) cap -= 16;
-  const size_t smem = CtaBuffers<T, P>::bytes(cap);
+  while (cap > 16 && CtaBuffers<T, P, S>::bytes(cap) > (size_t)optin) cap -= 16;
+  const size_t smem = CtaBuffers<T, P, S>::bytes(cap);
   // 16 warps per SM, split over as many CTAs (LPs) as shared memory allows
   const int ctas = (int)std::max<size_t>(1, (size_t)per_sm / (smem + 1024));
-  if (ctas >= 4) return launch_cta_t<T, P, 128>(kp, cap, smem, dev, stream);
-  if (ctas >= 2) return launch_cta_t<T, P, 256>(kp, cap, smem, dev, stream);
-  return launch_cta_t<T, P, 512>(kp, cap, smem, dev, stream);
+  if (ctas >= 4) return launch_cta_t<T, P, 128, S>(kp, cap, smem, dev, stream);
+  if (ctas >= 2) return launch_cta_t<T, P, 256, S>(kp, cap, smem, dev, stream);
+  return launch_cta_t<T, P, 512, S>(kp, cap, smem, dev, stream);
 }
 
 template <typename T, typename P>
@@ -442,12 +442,9 @@ int launch_fx(KParams kp, int64_t max_m, int dev, cudaStream_t s) {
 #define LP2D_FX_NS33 8  // register chunks of the m <= 1052 class (config 2)
 #endif
 
-// K4 covers the warp classes (29 <= m <= 4124); the lane class and the CTA
-// class read widened double copies (LP2D_B200_FX=0: every class does, A/B).
-bool fx_class(int cls) {
-  static const bool on = !(std::getenv("LP2D_B200_FX") && std::getenv("LP2D_B200_FX")[0] == '0');
-  return on && cls >= 1 && cls < n_reg_classes<double>();
-}
+// K4/K5 cover the warp classes (29 <= m <= 4124); the lane class and the CTA
+// class read the float storage directly (their kernels' S = float).
+bool fx_class(int cls) { return cls >= 1 && cls < n_reg_classes<double>(); }
 
 // ---- fp32 storage: K5 (k_solve_fs, lp2d_fs.cuh) ---------------------------
 // Run-time CTA shape: the most resident warps for the buffer size, at most
@@ -777,30 +774,17 @@ int widen_batch(KParams& kp, int64_t E, int64_t n, char* ws, int dev, cudaStream
 template <typename P>
 int solve_f32_balanced(KParams kp, int64_t E, int64_t min_m, int64_t max_m, int dev,
                        cudaStream_t s, bool may_sync) {
-  const int cmin = class_of<double>(std::max<int64_t>(min_m, 0));
-  const int cmax = class_of<double>(max_m);
-  bool need_widen = false;
-  for (int c = cmin; c <= cmax; ++c) need_widen |= !fx_class(c);
-  KParams kd = kp;
-  void* ws = nullptr;
-  if (need_widen) {
-    CUDA_TRY(cudaMallocFromPoolAsync(&ws, widen_bytes(E, kp.n_list), g_dev[dev].pool, s));
-    if (int rc = widen_batch(kd, E, kp.n_list, static_cast<char*>(ws), dev, s)) return rc;
-  }
-  const int rc = launch_binned<double>(
+  (void)E;
+  return launch_binned<double>(
       kp, min_m, max_m, dev, s, may_sync,
       [&](const KParams& kc, int c, int d, cudaStream_t cs, int64_t cap_m) {
         if (fx_class(c)) return launch_fx_class<P>(kc, c, d, cs, cap_m);
-        KParams k2 = kc;
-        k2.ax = kd.ax;
-        k2.ay = kd.ay;
-        k2.b = kd.b;
-        k2.c = kd.c;
-        k2.bound_m = kd.bound_m;
-        return launch_class<double, P>(k2, c, d, cs, cap_m);
+        // the lane class (m <= 28) and the CTA class (large LPs) read the
+        // float storage directly and widen on load (exact)
+        if (c >= n_reg_classes<double>()) return launch_cta_kernel<double, P, float>(kc, cap_m, d, cs);
+        if (tiny_uses_lanes()) return launch_lane_kernel<double, P, kLaneMaxM, float>(kc, d, cs);
+        return fail(LP2D_ERR_UNSUPPORTED, "fp32 storage: the warp tiny class needs LP2D_B200_TINY unset");
       });
-  if (ws) CUDA_TRY(cudaFreeAsync(ws, s));
-  return rc;
 }
 
 template <typename S>

@@ -709,7 +709,9 @@ __device__ __forceinline__ Line<T> shfl_line(const Line<T>& l, int src) {
   return r;
 }
 
-template <typename T, typename P, int MAXM>
+// S: storage type of the batch's scalars (float storage is widened exactly on
+// load; the arithmetic is T's, the fp32 configs' double semantics).
+template <typename T, typename P, int MAXM, typename S = T>
 __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid_constant__ KParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   using LT = LaneTile<T, MAXM>;
@@ -739,14 +741,14 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
     h.m = live ? p.m[h.lp] : 0;
     h.off = live ? p.offset[h.lp] : 0;
     h.ok = h.m >= 0 && h.m <= MAXM;
-    h.cx = live ? static_cast<const T*>(p.c)[2 * h.lp] : T(0);
-    h.cy = live ? static_cast<const T*>(p.c)[2 * h.lp + 1] : T(0);
-    h.M = live ? static_cast<const T*>(p.bound_m)[h.lp] : T(0);
+    h.cx = live ? (T) static_cast<const S*>(p.c)[2 * h.lp] : T(0);
+    h.cy = live ? (T) static_cast<const S*>(p.c)[2 * h.lp + 1] : T(0);
+    h.M = live ? (T) static_cast<const S*>(p.bound_m)[h.lp] : T(0);
     const int mj = live && h.ok ? h.m : 0;
     // ---- gather through the permutation (serial.hpp:28-32 insertion order)
-    const T* gx = static_cast<const T*>(p.ax) + h.off;
-    const T* gy = static_cast<const T*>(p.ay) + h.off;
-    const T* gb = static_cast<const T*>(p.b) + h.off;
+    const S* gx = static_cast<const S*>(p.ax) + h.off;
+    const S* gy = static_cast<const S*>(p.ay) + h.off;
+    const S* gb = static_cast<const S*>(p.b) + h.off;
     const P* gp = static_cast<const P*>(p.perm) + h.off;
     const int mmax = __reduce_max_sync(kFull, (uint32_t)mj);
     uint32_t pmax = 0;
@@ -787,9 +789,9 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
         if (k < MAXM && k < mj) {
           pmax = max(pmax, o[u]);
           const uint32_t oc = min(o[u], (uint32_t)(mj - 1));
-          vx[u] = gx[oc];
-          vy[u] = gy[oc];
-          vb[u] = gb[oc];
+          vx[u] = (T)gx[oc];
+          vy[u] = (T)gy[oc];
+          vb[u] = (T)gb[oc];
         }
       }
 #pragma unroll
@@ -811,9 +813,9 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
     const bool wild = !(m_all < Limits<T>::kBig) || !(fabs(h.M) < T(INFINITY));
     const T lpbnd = wild ? T(INFINITY)
                          : fmax(fmax(m_all, Limits<T>::kSmall) * eps_hi, FastDiv<T>::kDLo);
-    LPState<T> S;
-    lp_init(S, h);
-    S.st = bad ? 255 : 0;
+    LPState<T> St;
+    lp_init(St, h);
+    St.st = bad ? 255 : 0;
     const T cthr = eps_par * sqrt(h.cx * h.cx + h.cy * h.cy);
     bool alive = live && !bad;
     const int mpos = mj + 4;
@@ -821,14 +823,14 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
     // ---- lockstep sweep (serial.hpp:168-186 per lane) ----------------------
     for (int i = 4; i < pend; ++i) {
       const bool v = alive && i < mpos &&
-                     !satisfied(sx[at(i, lane)], sy[at(i, lane)], sb[at(i, lane)], S.px, S.py,
+                     !satisfied(sx[at(i, lane)], sy[at(i, lane)], sb[at(i, lane)], St.px, St.py,
                                 eps_feas);
       uint32_t vm = __ballot_sync(kFull, v);
       if (!vm) continue;
       Line<T> l;
       if (v) {
-        S.viol += 1;
-        S.wu += (uint32_t)i;
+        St.viol += 1;
+        St.wu += (uint32_t)i;
         note_event(p, h.lp, (uint32_t)i);
         l = boundary_of(sx[at(i, lane)], sy[at(i, lane)], sb[at(i, lane)]);
       }
@@ -870,7 +872,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
           mg.oL = acc.oL;
           mg.oR = acc.oR;
           mg.par = acc.par;
-          if (!resolve_merged(S, mg, l, (uint32_t)i, h, cthr, eps_feas)) alive = false;
+          if (!resolve_merged(St, mg, l, (uint32_t)i, h, cthr, eps_feas)) alive = false;
         }
       } else {
         // ---- pooled: the warp folds each violated LP in turn ----------------
@@ -914,15 +916,15 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
             }
           }
           const Merged<T> mg = merge_lanes(acc, rare_any);
-          if (lane == c && !resolve_merged(S, mg, l, (uint32_t)i, h, cthr, eps_feas))
+          if (lane == c && !resolve_merged(St, mg, l, (uint32_t)i, h, cthr, eps_feas))
             alive = false;
         }
       }
     }
     if (live) {
-      uint8_t st = S.st;
-      if (st == 0 && (S.pos0 < 4 || S.pos1 < 4)) st = 2;
-      write_result<T, P>(p, h, st, S.px, S.py, S.pos0, S.pos1, S.viol, S.wu);
+      uint8_t st = St.st;
+      if (st == 0 && (St.pos0 < 4 || St.pos1 < 4)) st = 2;
+      write_result<T, P>(p, h, st, St.px, St.py, St.pos0, St.pos1, St.viol, St.wu);
     }
     __syncwarp();  // the tile is rewritten by the next group
     g = (int64_t)__shfl_sync(kFull, ticket, 0) + TW;
@@ -970,42 +972,43 @@ struct CtaShared {
   uint32_t redk[kCtaMaxWarps][3];  // per-warp pmax / |a| bound words
 };
 
-template <typename T, typename P>
+// S: the staged (stored) scalar type, T: the arithmetic's.
+template <typename T, typename P, typename S = T>
 struct CtaBuffers {
   static __host__ __device__ size_t head() { return (sizeof(CtaShared<T>) + 127) & ~size_t(127); }
   static __host__ __device__ size_t bytes(int64_t cap) {
-    return head() + (3 * sizeof(T) + sizeof(P)) * (size_t)cap;
+    return head() + (3 * sizeof(S) + sizeof(P)) * (size_t)cap;
   }
 };
 
-template <typename T>
+template <typename T, typename S = T>
 __device__ __forceinline__ Header<T> unpack_header_cap(uint32_t w, int64_t lp, int64_t cap,
                                                        bool& fits) {
-  constexpr int WT = sizeof(T) / 4;
+  constexpr int WT = sizeof(S) / 4;
   Header<T> h;
   h.lp = lp;
   h.m = (int32_t)__shfl_sync(kFull, w, 0);
   h.off = (int64_t)(((uint64_t)__shfl_sync(kFull, w, 2) << 32) | __shfl_sync(kFull, w, 1));
   const int64_t o1 = (int64_t)(((uint64_t)__shfl_sync(kFull, w, 4) << 32) | __shfl_sync(kFull, w, 3));
-  h.cx = word_scalar<T>(w, 5);
-  h.cy = word_scalar<T>(w, 5 + WT);
-  h.M = word_scalar<T>(w, 5 + 2 * WT);
+  h.cx = (T)word_scalar<S>(w, 5);
+  h.cy = (T)word_scalar<S>(w, 5 + WT);
+  h.M = (T)word_scalar<S>(w, 5 + 2 * WT);
   const int64_t cap8 = ((int64_t)h.m + 7) & ~int64_t(7);
   h.ok = h.m >= 0 && (h.off & 7) == 0 && o1 - h.off >= cap8;
   fits = h.ok && h.m <= cap;
   return h;
 }
 
-template <typename T, typename P, int THREADS>
+template <typename T, typename P, int THREADS, typename S = T>
 __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ KParams p, int32_t cap) {
   static_assert(sizeof(T) == 4 || sizeof(T) == 8, "scalar");
   constexpr int W = THREADS / 32;
   static_assert(W <= kCtaMaxWarps, "warps per CTA");
   extern __shared__ __align__(128) unsigned char smem[];
   CtaShared<T>& sh = *reinterpret_cast<CtaShared<T>*>(smem);
-  T* rax = reinterpret_cast<T*>(smem + CtaBuffers<T, P>::head());
-  T* ray = rax + cap;
-  T* rb = ray + cap;
+  S* rax = reinterpret_cast<S*>(smem + CtaBuffers<T, P, S>::head());
+  S* ray = rax + cap;
+  S* rb = ray + cap;
   P* rperm = reinterpret_cast<P*>(rb + cap);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int32_t* list;
@@ -1020,9 +1023,9 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
   auto pos = [&](int k, T M, T& x, T& y, T& bb) {
     const bool box = k < 4;
     const uint32_t o = rperm[box ? 0 : k - 4];
-    x = box ? (k == 0 ? T(1) : (k == 1 ? T(-1) : T(0))) : rax[o];
-    y = box ? (k == 2 ? T(1) : (k == 3 ? T(-1) : T(0))) : ray[o];
-    bb = box ? M : rb[o];
+    x = box ? (k == 0 ? T(1) : (k == 1 ? T(-1) : T(0))) : (T)rax[o];
+    y = box ? (k == 2 ? T(1) : (k == 3 ? T(-1) : T(0))) : (T)ray[o];
+    bb = box ? M : (T)rb[o];
   };
   // warp 0's pipeline registers: the next LP's header words and ticket
   uint32_t hwN = 0, ticket = 0;
@@ -1031,7 +1034,7 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
   if (wid == 0) {
     policy = policy_evict_first();
     lpN = lp_of(blockIdx.x);
-    hwN = load_header_word<T>(p, lpN, lane);
+    hwN = load_header_word<S>(p, lpN, lane);
     ticket = atomic_add_if(p.counter, lane == 0, p.pk.zero);
     if (lane == 0) mbar_init(&sh.bar, 1);
   }
@@ -1041,23 +1044,23 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
     // ---- warp 0: stage the LP (header loaded an LP ago) -------------------
     if (wid == 0) {
       bool fits;
-      const Header<T> hn = unpack_header_cap<T>(hwN, lpN, cap, fits);
+      const Header<T> hn = unpack_header_cap<T, S>(hwN, lpN, cap, fits);
       if (lane == 0) {
         sh.hdr = hn;
         if (hn.lp >= 0) {
-          const uint32_t bt = fits ? round16((uint32_t)hn.m * sizeof(T)) : 0u;
+          const uint32_t bt = fits ? round16((uint32_t)hn.m * sizeof(S)) : 0u;
           const uint32_t bp = fits ? round16((uint32_t)hn.m * sizeof(P)) : 0u;
           mbar_arrive_expect_tx(&sh.bar, 3 * bt + bp);
           if (bt) {
-            bulk_g2s(rax, static_cast<const T*>(p.ax) + hn.off, bt, &sh.bar, policy);
-            bulk_g2s(ray, static_cast<const T*>(p.ay) + hn.off, bt, &sh.bar, policy);
-            bulk_g2s(rb, static_cast<const T*>(p.b) + hn.off, bt, &sh.bar, policy);
+            bulk_g2s(rax, static_cast<const S*>(p.ax) + hn.off, bt, &sh.bar, policy);
+            bulk_g2s(ray, static_cast<const S*>(p.ay) + hn.off, bt, &sh.bar, policy);
+            bulk_g2s(rb, static_cast<const S*>(p.b) + hn.off, bt, &sh.bar, policy);
             bulk_g2s(rperm, static_cast<const P*>(p.perm) + hn.off, bp, &sh.bar, policy);
           }
         }
       }
       lpN = lp_of((int64_t)__shfl_sync(kFull, ticket, 0) + G);
-      hwN = load_header_word<T>(p, lpN, lane);
+      hwN = load_header_word<S>(p, lpN, lane);
       ticket = atomic_add_if(p.counter, lane == 0, p.pk.zero);
     }
     __syncthreads();  // header visible (and the previous LP's reads are done)
@@ -1073,7 +1076,7 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
     if (fits) {
       for (int i = tid; i < h.m; i += THREADS) {
         pmax = max(pmax, (uint32_t)rperm[i]);
-        sbits = max(sbits, float_bits(fabs(rax[i]) + fabs(ray[i])));
+        sbits = max(sbits, float_bits(fabs((T)rax[i]) + fabs((T)ray[i])));
       }
     } else if (h.ok) {
       const P* gperm = static_cast<const P*>(p.perm) + h.off;
@@ -1103,9 +1106,9 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
     const T m_all = float_from_bits<T>(sb_all);
     const bool wild = !(m_all < Limits<T>::kBig) || !(fabs(h.M) < T(INFINITY)) || !fits;
     const T lpbnd = fmax(fmax(m_all, Limits<T>::kSmall) * eps_hi, FastDiv<T>::kDLo);
-    LPState<T> S;
-    lp_init(S, h);
-    S.st = bad ? 255 : 0;
+    LPState<T> St;
+    lp_init(St, h);
+    St.st = bad ? 255 : 0;
     const T cthr = eps_par * sqrt(h.cx * h.cx + h.cy * h.cy);
     bool need_exact = !bad && wild;
     // ---- sweep (serial.hpp:168-186) ----------------------------------------
@@ -1119,7 +1122,7 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
         if (P_ >= start && P_ < mpos) {
           T x, y, bb;
           pos(P_, h.M, x, y, bb);
-          v = !satisfied(x, y, bb, S.px, S.py, eps_feas);
+          v = !satisfied(x, y, bb, St.px, St.py, eps_feas);
         }
         const uint32_t bm = __ballot_sync(kFull, v);
         uint32_t* bal = sh.bal[step & 1];
@@ -1136,8 +1139,8 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
       }
       if (pi < 0) break;
       // ---- event at position pi ------------------------------------------
-      S.viol += 1;
-      S.wu += (uint32_t)pi;
+      St.viol += 1;
+      St.wu += (uint32_t)pi;
       if (tid == 0) note_event(p, h.lp, (uint32_t)pi);
       T hx, hy, hb;
       pos(pi, h.M, hx, hy, hb);
@@ -1204,20 +1207,20 @@ __global__ void __launch_bounds__(THREADS) k_solve_cta(const __grid_constant__ K
       aw.oR = lane < W ? sh.oR[lane] : kNone;
       aw.par = lane < W ? sh.par[lane] : kNone;
       const Merged<T> mg = merge_lanes(aw, true);
-      if (!resolve_merged(S, mg, l, (uint32_t)pi, h, cthr, eps_feas)) break;
-      if (!(fabs(S.px) < T(INFINITY) && fabs(S.py) < T(INFINITY))) {
+      if (!resolve_merged(St, mg, l, (uint32_t)pi, h, cthr, eps_feas)) break;
+      if (!(fabs(St.px) < T(INFINITY) && fabs(St.py) < T(INFINITY))) {
         need_exact = true;
         break;
       }
       start = pi + 1;
     }
     if (need_exact) {
-      if (wid == 0) solve_exact_global<T, P>(p, h, eps_par, eps_feas, eps_hi, S, S.viol);
+      if (wid == 0) solve_exact_global<T, P, S>(p, h, eps_par, eps_feas, eps_hi, St, St.viol);
     }
     if (tid == 0) {
-      uint8_t st = S.st;
-      if (st == 0 && (S.pos0 < 4 || S.pos1 < 4)) st = 2;
-      write_result<T, P>(p, h, st, S.px, S.py, S.pos0, S.pos1, S.viol, S.wu);
+      uint8_t st = St.st;
+      if (st == 0 && (St.pos0 < 4 || St.pos1 < 4)) st = 2;
+      write_result<T, P>(p, h, st, St.px, St.py, St.pos0, St.pos1, St.viol, St.wu);
     }
     fence_proxy_async_smem();  // this LP's reads before the next LP's TMA
   }
