@@ -209,44 +209,76 @@ def config_dtype(cfg_name, dtype_arg):
     return dt
 
 
-def make_batch(cfg_name, rank, dt, via="ours"):
-    """SURVEY.md §8(d) workloads; LP j of rank r is global LP r*n + j.
-    via="ours": the product's generator (lp2dgen_fill); via="reference": the
-    reference's own generator (oracle/_ref ref_fill), so the reference arm
-    never loads the product library. Both give the same instance bit for bit
-    (tests/test_generate.py)."""
-    n, m, _, seed, _ = CONFIGS[cfg_name]
+# Full sizes of the configs BASELINE.json quotes "sharded over 8 GPUs":
+# --full puts the whole config on this job's GPUs (strong scaling).
+FULL = {"c3": 1 << 20, "c5": 1 << 22}
+E2E_CAP = 1 << 19    # --full: the e2e leg times this many LPs per rank (host RAM)
+CPU_CAP = 1 << 15    # --full: the CPU baseline's bounded sample
+
+
+def config_layout(cfg_name, first, n=None, via="ours"):
+    """(sizes, kind, bscale, seed) of global LPs [first, first + n) of a
+    config; n defaults to the per-GPU shard size."""
+    n0, m, _, seed, _ = CONFIGS[cfg_name]
     kind, bscale = None, 1.0
     if cfg_name == "c4":
         sizes = pareto_sizes(seed, via=via)
-        n = len(sizes)
     else:
-        sizes = np.full(n, m, np.int32)
-    g = np.arange(rank * n, (rank + 1) * n)
+        sizes = np.full(n0 if n is None else n, m, np.int32)
+    g = np.arange(first, first + len(sizes))
     FEAS, INF, UNB = 0, 1, 3  # generate.hpp gen_kind (+ the builder's unbounded kind)
     if cfg_name == "c3":
         kind = np.where(g % 10 == 0, INF, FEAS).astype(np.uint8)
         bscale = 2e-7
     elif cfg_name == "c5":
-        kind = np.full(n, FEAS, np.uint8)
+        kind = np.full(len(sizes), FEAS, np.uint8)
         kind[g % 10 == 3] = INF
         kind[g % 10 == 7] = UNB
+    return sizes, kind, bscale, seed
+
+
+def make_batch(cfg_name, rank, dt, via="ours", n=None, first=None):
+    """SURVEY.md §8(d) workloads; LP j of rank r is global LP r*n + j.
+    via="ours": the product's generator (lp2dgen_fill); via="reference": the
+    reference's own generator (oracle/_ref ref_fill), so the reference arm
+    never loads the product library. Both give the same instance bit for bit
+    (tests/test_generate.py)."""
+    n_cfg = CONFIGS[cfg_name][0]
+    if first is None:
+        first = rank * (n if n is not None else n_cfg)
+    sizes, kind, bscale, seed = config_layout(cfg_name, first, n, via)
     if via == "reference":
-        pb = _oracle().ref_fill(sizes, seed, kind=kind, bscale=bscale, first=rank * n)
+        pb = _oracle().ref_fill(sizes, seed, kind=kind, bscale=bscale, first=first)
         pb.perm = pb.perm.astype(np.uint16) if pb.m.max(initial=0) <= 65536 else pb.perm
     else:
         import paper_1902_04995_b200 as P
 
-        pb = P.PackedBatch.generate(sizes, seed, first=rank * n, kind=kind, bscale=bscale)
+        pb = P.PackedBatch.generate(sizes, seed, first=first, kind=kind, bscale=bscale)
     return pb.astype(dt) if dt != np.float64 else pb
 
 
-def config_dict(cfg_name, pb, world, dt):
+def make_device_batch(cfg_name, first, n, dt, device):
+    """The same workload synthesised on the GPU (lp2dgpu_generate_device:
+    the host generator's integer streams; cos/sin from CUDA's libm)."""
+    import paper_1902_04995_b200 as P
+
+    sizes, kind, bscale, seed = config_layout(cfg_name, first, n)
+    return P.DeviceBatch.generate(sizes, seed, kind=kind, bscale=bscale, first=first,
+                                  dtype=dt, device=device)
+
+
+def config_dict(cfg_name, pb, world, dt, full=False):
     """The `config` object of both arms' JSON lines (identical keys/values)."""
-    n, m = pb.n, CONFIGS[cfg_name][1] or float(np.mean(pb.m))
-    return {"workload": CONFIGS[cfg_name][4], "config": cfg_name, "lps_per_gpu": int(n),
-            "m": m, "storage": "f32" if dt == np.float32 else "f64", "arithmetic": "f64",
-            "parallelism": "dp%d (LP-index shards, no collective)" % world}
+    full = full and cfg_name in FULL
+    n = FULL[cfg_name] // world if full else CONFIGS[cfg_name][0] or pb.n
+    m = CONFIGS[cfg_name][1] or float(np.mean(pb.m))
+    d = {"workload": CONFIGS[cfg_name][4], "config": cfg_name, "lps_per_gpu": int(n),
+         "m": m, "storage": "f32" if dt == np.float32 else "f64", "arithmetic": "f64",
+         "parallelism": "dp%d (LP-index shards, no collective)" % world}
+    if full:
+        d["workload"] = "FULL %s: %d LPs on %d GPU(s)" % (cfg_name, FULL[cfg_name], world)
+        d["total_lps"] = FULL[cfg_name]
+    return d
 
 
 def cpu_model():
@@ -302,15 +334,19 @@ def run_reference_arm(args, world, rank):
     if rank != 0:
         return
     dt = config_dtype(cfg, args.dtype)
-    pb = make_batch(cfg, 0, dt, via="reference")
+    full = args.full and cfg in FULL
+    # --full: each step is a bounded sample of the full workload (same LPs/s)
+    pb = make_batch(cfg, 0, dt, via="reference", n=CPU_CAP if full else None, first=0)
     n = pb.n
     cb = cpu_reference(pb, args.steps, args.warmup)
+    if full:
+        cb["sample"] += f" (sample of the {FULL[cfg]}-LP full config)"
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "LPs/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * n / cb["value"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA % CONFIGS[cfg][3],
-        "config": config_dict(cfg, pb, world, dt),
+        "config": config_dict(cfg, pb, world, dt, full),
         "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": "LPs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -335,6 +371,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 5)")
     ap.add_argument("--streams", type=int, default=2,
                     help="streams the K timed steps alternate over (1 = back-to-back)")
+    ap.add_argument("--full", action="store_true",
+                    help="c3/c5: the config's full size (2^20 / 2^22 LPs) split over this "
+                         "job's GPUs (strong scaling), synthesised on the device")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_env()
@@ -366,12 +405,21 @@ def main():
     cfg = args.config
     _, m, _, seed, desc = CONFIGS[cfg]
     dt = config_dtype(cfg, args.dtype)
-    pb = make_batch(cfg, rank, dt)
-    n, m = pb.n, (m or int(pb.m.mean()))
-    algo_bytes = pb.constraint_bytes()
+    full = args.full and cfg in FULL
+    if full:
+        n = FULL[cfg] // world
+        db = make_device_batch(cfg, rank * n, n, dt, local)
+        # host copies of a bounded sample for the e2e leg / CPU baseline
+        pb = make_batch(cfg, rank, dt, n=min(n, E2E_CAP), first=rank * n)
+        algo_bytes = db.constraint_bytes
+    else:
+        pb = make_batch(cfg, rank, dt)
+        n = pb.n
+        db = P.DeviceBatch(pb, device=local)
+        algo_bytes = pb.constraint_bytes()
+    m = m or int(pb.m.mean())
 
     # ---- device-resident kernel timing ----------------------------------------
-    db = P.DeviceBatch(pb, device=local)
     out = db.empty_result()
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -436,19 +484,21 @@ def main():
 
     # ---- naive scheduler on the same device batch (paper's RGB-naive vs
     # balanced comparison) ------------------------------
-    naive = P.BlockConfig(scheduler=P.SchedulerKind.naive)
-    for _ in range(2):
-        P.solve_device(db, out, naive, stream=stream)
-    ne0 = torch.cuda.Event(enable_timing=True)
-    ne1 = torch.cuda.Event(enable_timing=True)
-    nsteps = 3
-    ne0.record(stream)
-    for _ in range(nsteps):
-        P.solve_device(db, out, naive, stream=stream)
-    ne1.record(stream)
-    torch.cuda.synchronize()
-    naive_ms = ne0.elapsed_time(ne1) / nsteps
-    P.solve_device(db, out, stream=stream)  # leave balanced results in `out`
+    naive_ms = None
+    if not full:  # (a comparison leg: skipped at the full sizes)
+        naive = P.BlockConfig(scheduler=P.SchedulerKind.naive)
+        for _ in range(2):
+            P.solve_device(db, out, naive, stream=stream)
+        ne0 = torch.cuda.Event(enable_timing=True)
+        ne1 = torch.cuda.Event(enable_timing=True)
+        nsteps = 3
+        ne0.record(stream)
+        for _ in range(nsteps):
+            P.solve_device(db, out, naive, stream=stream)
+        ne1.record(stream)
+        torch.cuda.synchronize()
+        naive_ms = ne0.elapsed_time(ne1) / nsteps
+        P.solve_device(db, out, stream=stream)  # leave balanced results in `out`
 
     # ---- end-to-end through the C ABI with pinned host buffers ---------------
     e2e_steps = args.e2e_steps or min(args.steps, 5)
@@ -470,7 +520,7 @@ def main():
     te1 = time.perf_counter()
     barrier()
     e2e_s = max_over_ranks(te1 - te0)
-    e2e_value = world * n * e2e_steps / e2e_s
+    e2e_value = world * pb.n * e2e_steps / e2e_s
 
     # ---- rank-0 extras: parity spot check, cpu baseline, JSON line ------------
     if rank == 0:
@@ -479,18 +529,22 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "LPs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "storage": "f32" if dt == np.float32 else "f64",
-            "data": DATA % seed,
-            "config": config_dict(cfg, pb, world, dt),
-            "l2": "inputs %.0f MB %s 126 MB L2, no flush" % (h2d / 1e6, ">" if h2d > 126e6 else "<"),
+            "higher_is_better": True, "scaling": "strong" if full else "weak",
+            "vs_baseline": None, "dtype": "f64", "storage": "f32" if dt == np.float32 else "f64",
+            "data": (DATA % seed) + ("; synthesised on the device (the same integer streams, "
+                                     "CUDA cos/sin)" if full else ""),
+            "config": config_dict(cfg, pb, world, dt, full),
+            "l2": "constraints %.0f MB %s 126 MB L2, no flush" % (
+                algo_bytes / 1e6, ">" if algo_bytes > 126e6 else "<"),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": load_traffic(cfg),
+                         "frac": achieved / peak,
+                         "traffic": None if full else load_traffic(cfg),
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": algo_bytes,
                          "kernel_ms": kern_ms_max},
             "e2e": {"value": e2e_value, "unit": "LPs/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
+                    "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+                    "lps_per_step": int(world * pb.n)},
             "gpu_launches": launches_p,
             "pipeline": {"streams": ns, "ms_per_step": ms_per_step,
                          "single_stream_ms_per_step": single_ms_per_step,
@@ -503,7 +557,7 @@ def main():
                                  "one's ramp-up; roofline: isolated launches of the "
                                  "single-stream loop"},
             "schedulers": {"balanced_kernel_ms": kern_ms, "naive_kernel_ms": naive_ms,
-                           "naive_over_balanced": naive_ms / kern_ms,
+                           "naive_over_balanced": naive_ms / kern_ms if naive_ms else None,
                            "note": "naive = thread per LP (paper's RGB naive), balanced = "
                                    "warp-dealt work units (this kernel); same device batch"},
             "clocks": clk2.summary(),
@@ -511,7 +565,8 @@ def main():
         if not args.no_cpu_baseline:
             try:
                 # ~1 s wall on all host cores (x cores = 10-30 s of CPU work)
-                line["cpu_baseline"] = cpu_reference(pb, steps=8, warmup=1)
+                line["cpu_baseline"] = cpu_reference(
+                    pb.subset(0, min(pb.n, CPU_CAP)) if full else pb, steps=8, warmup=1)
             except Exception as e:  # reference .so absent on this box
                 line["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
         print(json.dumps(line), flush=True)
