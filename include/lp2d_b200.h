@@ -51,6 +51,10 @@ enum {
   LP2D_INFEASIBLE = 1,  /* solution::infeasible()                            */
   LP2D_UNBOUNDED = 2,   /* feasible, optimum held by a box edge (k < 4)      */
   LP2D_INVALID = 255,   /* malformed input for this LP (perm out of range)   */
+  LP2D_MOCK = 254,      /* test-only mock devices (LP2D_B200_MOCK_DEVICES=N):
+                           the host-mode shard/chunk driver ran without CUDA;
+                           x = global LP index, y = shard, value = the chunk's
+                           first LP, work_units = m. Not a solution.        */
 };
 /* pair entries: original constraint index, box position k -> -(k+1),
  * LP2D_PAIR_NONE when no constraint owns the endpoint. */
@@ -128,9 +132,13 @@ typedef struct lp2d_out {
 
 void lp2dgpu_default_opts(lp2d_opts* opts);
 
-/* Solve a batch. Host mode: copies in, solves (sharded over n_gpus devices,
- * one host thread per device) and copies out before returning. Device mode:
- * enqueues on opts->stream and returns without synchronising. */
+/* Solve a batch. Host mode: shards the batch over n_gpus devices (LP ranges
+ * balanced by sum(m + 4), one host thread per device); each shard is cut into
+ * chunks (LP2D_B200_CHUNK_ELEMS elements, default 16 Mi) pipelined over two
+ * device slots (H2D of the next chunk overlaps the solve of the current one;
+ * pageable inputs are staged through pinned buffers, pinned ones are DMA'd
+ * directly); returns when every result is in place. Device mode: enqueues on
+ * opts->stream and returns without synchronising. */
 int lp2dgpu_solve_f32(const lp2d_batch_soa* batch, const lp2d_opts* opts,
                       lp2d_out* out);
 int lp2dgpu_solve_f64(const lp2d_batch_soa* batch, const lp2d_opts* opts,

@@ -807,120 +807,307 @@ int solve_device_batch(KParams kp, int64_t E, int64_t min_m, int64_t max_m, int 
 }
 
 // ---- host mode: one shard [lo, hi) on one device ----------------------------
+// The shard is cut into chunks of at most chunk_elems() constraint elements
+// and pipelined over two device slots: H2D of chunk k+1 (copy stream) runs
+// while chunk k is solved (compute stream), and chunk k's results come back
+// on the copy stream behind chunk k+1's inputs. Inputs in pageable memory are
+// staged through two pinned buffers (filled by this shard's host thread while
+// the previous chunk's DMA runs); pinned (page-locked / registered) inputs are
+// DMA'd directly. Results go to pinned staging and are copied out after their
+// D2H completes, or straight into pinned result buffers.
+
+int64_t chunk_elems() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("LP2D_B200_CHUNK_ELEMS");
+    const long long x = e ? std::atoll(e) : 0;
+    return x > 0 ? (int64_t)x : (int64_t)(16 << 20);
+  }();
+  return v;
+}
+
+// Chunk boundaries of [lo, hi): consecutive LP ranges spanning at most
+// max_elems elements of the packed arrays (at least one LP each).
+std::vector<int64_t> plan_chunks(const int64_t* offset, int64_t lo, int64_t hi, int64_t max_elems) {
+  std::vector<int64_t> cut{lo};
+  int64_t start = lo;
+  while (start < hi) {
+    // last j in (start, hi] with offset[j] - offset[start] <= max_elems
+    const int64_t* f = std::upper_bound(offset + start + 1, offset + hi + 1, offset[start] + max_elems);
+    int64_t j = (int64_t)(f - offset) - 1;
+    if (j <= start) j = start + 1;
+    cut.push_back(j);
+    start = j;
+  }
+  return cut;
+}
+
+// Test-only mock devices (LP2D_B200_MOCK_DEVICES=N, N >= 1): host mode runs
+// the threaded shard driver and the chunk planner without CUDA, and every LP
+// gets status LP2D_MOCK with x = its global index, y = its shard, value = its
+// chunk's first LP, work_units = its m (the gather order is checkable on a
+// machine without a GPU). Never set in production: results are not solutions.
+int mock_devices() {
+  static const int v = [] {
+    const char* e = std::getenv("LP2D_B200_MOCK_DEVICES");
+    return e ? std::max(0, std::atoi(e)) : 0;
+  }();
+  return v;
+}
+
+bool host_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Per-device host-mode resources (grown on demand, kept across calls).
+struct HostPipe {
+  cudaStream_t copy = nullptr;
+  cudaEvent_t h2d[2] = {}, solved[2] = {}, d2h[2] = {};
+  void* pin_in[2] = {};
+  size_t pin_in_bytes = 0;
+  void* pin_out[2] = {};
+  size_t pin_out_bytes = 0;
+};
+HostPipe g_pipe[64];
+
+int ensure_pinned(void** slot, size_t& have, size_t want) {
+  if (have >= want) return 0;
+  for (int q = 0; q < 2; ++q) {
+    if (slot[q]) CUDA_TRY(cudaFreeHost(slot[q]));
+    slot[q] = nullptr;
+  }
+  have = 0;
+  for (int q = 0; q < 2; ++q) CUDA_TRY(cudaHostAlloc(&slot[q], want, cudaHostAllocDefault));
+  have = want;
+  return 0;
+}
+
+template <typename S>
+int solve_shard_mock(int dev, const lp2d_batch_soa* b, lp2d_out* out, int64_t lo, int64_t hi) {
+  const std::vector<int64_t> cut = plan_chunks(b->offset, lo, hi, chunk_elems());
+  for (size_t k = 0; k + 1 < cut.size(); ++k)
+    for (int64_t j = cut[k]; j < cut[k + 1]; ++j) {
+      out->status[j] = LP2D_MOCK;
+      static_cast<double*>(out->x)[j] = (double)j;
+      static_cast<double*>(out->y)[j] = (double)dev;
+      static_cast<double*>(out->value)[j] = (double)cut[k];
+      if (out->work_units) out->work_units[j] = (uint64_t)b->m[j];
+    }
+  return 0;
+}
+
 template <typename S>
 int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out,
                      int64_t lo, int64_t hi, int64_t min_m, int64_t max_m) {
   using T = double;  // outputs
+  if (mock_devices()) return solve_shard_mock<S>(dev, b, out, lo, hi);
   if (int rc = ensure_device(dev)) return rc;
   DeviceState& d = g_dev[dev];
   std::lock_guard<std::mutex> lock(d.mu);
   CUDA_TRY(cudaSetDevice(dev));
-  const int64_t cnt = hi - lo;
-  const int64_t e0 = b->offset[lo], e1 = b->offset[hi];
-  const int64_t E = e1 - e0;
+  HostPipe& hp = g_pipe[dev];
+  if (!hp.copy) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&hp.copy, cudaStreamNonBlocking));
+    for (int q = 0; q < 2; ++q) {
+      CUDA_TRY(cudaEventCreateWithFlags(&hp.h2d[q], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&hp.solved[q], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&hp.d2h[q], cudaEventDisableTiming));
+    }
+  }
+  const std::vector<int64_t> cut = plan_chunks(b->offset, lo, hi, chunk_elems());
+  const int nk = (int)cut.size() - 1;
+  int64_t cmax = 0, emax = 0;
+  for (int k = 0; k < nk; ++k) {
+    cmax = std::max(cmax, cut[k + 1] - cut[k]);
+    emax = std::max(emax, b->offset[cut[k + 1]] - b->offset[cut[k]]);
+  }
   const size_t ps = b->perm_bits / 8;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  size_t off_m = 0;
-  size_t off_offset = off_m + al(sizeof(int32_t) * cnt);
-  size_t off_ax = off_offset + al(sizeof(int64_t) * (cnt + 1));
-  size_t off_ay = off_ax + al(sizeof(S) * E);
-  size_t off_b = off_ay + al(sizeof(S) * E);
-  size_t off_perm = off_b + al(sizeof(S) * E);
-  size_t off_c = off_perm + al(ps * E);
-  size_t off_M = off_c + al(sizeof(S) * 2 * cnt);
-  size_t off_st = off_M + al(sizeof(S) * cnt);
-  size_t off_x = off_st + al(cnt);
-  size_t off_y = off_x + al(sizeof(T) * cnt);
-  size_t off_v = off_y + al(sizeof(T) * cnt);
-  size_t off_pair = off_v + al(sizeof(T) * cnt);
-  size_t off_viol = off_pair + al(sizeof(int32_t) * 2 * cnt);
-  size_t off_wu = off_viol + al(sizeof(uint32_t) * cnt);
-  // (lane_stats histogram: the rows of the blocks this shard touches)
+  // one slot: inputs (the contiguous pinned/staged part first) + outputs
+  size_t o_in = 0;
+  const size_t o_ax = 0, o_ay = o_ax + al(sizeof(S) * emax), o_b = o_ay + al(sizeof(S) * emax);
+  const size_t o_perm = o_b + al(sizeof(S) * emax), o_c = o_perm + al(ps * emax);
+  const size_t o_M = o_c + al(sizeof(S) * 2 * cmax), o_m = o_M + al(sizeof(S) * cmax);
+  const size_t o_off = o_m + al(sizeof(int32_t) * cmax);
+  const size_t in_bytes = o_off + al(sizeof(int64_t) * (cmax + 1));
+  o_in = in_bytes;
+  const size_t r_st = 0, r_x = r_st + al(cmax), r_y = r_x + al(sizeof(T) * cmax);
+  const size_t r_v = r_y + al(sizeof(T) * cmax), r_pair = r_v + al(sizeof(T) * cmax);
+  const size_t r_viol = r_pair + al(sizeof(int32_t) * 2 * cmax);
+  const size_t r_wu = r_viol + al(sizeof(uint32_t) * cmax);
+  const size_t out_bytes = r_wu + al(sizeof(uint64_t) * cmax);
+  // (lane_stats histogram rows of the blocks one chunk touches)
   const int64_t W = o->block_width;
-  const int64_t row0 = lo / W, rows = out->iter_hist ? (hi - 1) / W - row0 + 1 : 0;
   const int64_t hstride = max_m + 1;
-  size_t off_hist = off_wu + al(sizeof(uint64_t) * cnt);
-  size_t total = off_hist + al(sizeof(uint32_t) * rows * hstride);
-  if (d.arena_bytes < total) {
+  const int64_t hrows = out->iter_hist ? cmax / W + 2 : 0;
+  const size_t hist_bytes = al(sizeof(uint32_t) * hrows * hstride);
+  const size_t slot_bytes = in_bytes + out_bytes + hist_bytes;
+  if (d.arena_bytes < 2 * slot_bytes) {
     if (d.arena) CUDA_TRY(cudaFree(d.arena));
     d.arena = nullptr;
     d.arena_bytes = 0;
-    CUDA_TRY(cudaMalloc(&d.arena, total));
-    d.arena_bytes = total;
+    CUDA_TRY(cudaMalloc(&d.arena, 2 * slot_bytes));
+    d.arena_bytes = 2 * slot_bytes;
   }
-  char* A = static_cast<char*>(d.arena);
-  cudaStream_t s = d.stream;
-  std::vector<int64_t> offs(cnt + 1);
-  for (int64_t j = 0; j <= cnt; ++j) offs[j] = b->offset[lo + j] - e0;
-  CUDA_TRY(cudaMemcpyAsync(A + off_m, b->m + lo, sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(A + off_offset, offs.data(), sizeof(int64_t) * (cnt + 1),
-                           cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(A + off_ax, static_cast<const S*>(b->ax) + e0, sizeof(S) * E,
-                           cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(A + off_ay, static_cast<const S*>(b->ay) + e0, sizeof(S) * E,
-                           cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(A + off_b, static_cast<const S*>(b->b) + e0, sizeof(S) * E,
-                           cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(A + off_perm, static_cast<const char*>(b->perm) + ps * e0, ps * E,
-                           cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(A + off_c, static_cast<const S*>(b->c) + 2 * lo, sizeof(S) * 2 * cnt,
-                           cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(A + off_M, static_cast<const S*>(b->bound_m) + lo, sizeof(S) * cnt,
-                           cudaMemcpyHostToDevice, s));
-  KParams kp = make_params<T>(o);
-  kp.n_list = cnt;
-  kp.list = nullptr;
-  kp.m = reinterpret_cast<const int32_t*>(A + off_m);
-  kp.offset = reinterpret_cast<const int64_t*>(A + off_offset);
-  kp.ax = A + off_ax;
-  kp.ay = A + off_ay;
-  kp.b = A + off_b;
-  kp.perm = A + off_perm;
-  kp.c = A + off_c;
-  kp.bound_m = A + off_M;
-  kp.status = reinterpret_cast<uint8_t*>(A + off_st);
-  kp.x = A + off_x;
-  kp.y = A + off_y;
-  kp.value = A + off_v;
-  kp.pair = reinterpret_cast<int32_t*>(A + off_pair);
-  kp.viol = reinterpret_cast<uint32_t*>(A + off_viol);
-  kp.wu = reinterpret_cast<uint64_t*>(A + off_wu);
-  if (rows) {
-    kp.iter_hist = reinterpret_cast<uint32_t*>(A + off_hist);
-    kp.hist_lp0 = lo - row0 * W;  // local LP 0 sits at this offset within row 0
-    kp.hist_w = (int32_t)W;
-    kp.hist_stride = (int32_t)hstride;
-    CUDA_TRY(cudaMemsetAsync(kp.iter_hist, 0, sizeof(uint32_t) * rows * hstride, s));
+  const bool in_pinned = host_pinned(b->ax) && host_pinned(b->ay) && host_pinned(b->b) &&
+                         host_pinned(b->perm) && host_pinned(b->c) && host_pinned(b->bound_m);
+  const bool out_pinned = host_pinned(out->status) && host_pinned(out->x) && host_pinned(out->y) &&
+                          host_pinned(out->value) && host_pinned(out->pair) &&
+                          host_pinned(out->violation_events) && host_pinned(out->work_units);
+  // the small per-chunk arrays (m, rebased offsets) always go through staging
+  if (int rc = ensure_pinned(hp.pin_in, hp.pin_in_bytes, in_pinned ? al(o_in - o_m) : in_bytes)) return rc;
+  if (!out_pinned)
+    if (int rc = ensure_pinned(hp.pin_out, hp.pin_out_bytes, out_bytes + hist_bytes)) return rc;
+  cudaStream_t cs = d.stream, cp = hp.copy;
+  char* arena = static_cast<char*>(d.arena);
+  std::vector<std::vector<uint32_t>> hist_host(2);
+
+  // stage + enqueue the H2D of chunk k into slot k % 2
+  auto upload = [&](int k) -> int {
+    const int q = k & 1;
+    const int64_t c0 = cut[k], c1 = cut[k + 1], cnt = c1 - c0;
+    const int64_t e0 = b->offset[c0], E = b->offset[c1] - e0;
+    char* D = arena + q * slot_bytes;
+    char* H = static_cast<char*>(hp.pin_in[q]);
+    CUDA_TRY(cudaEventSynchronize(hp.h2d[q]));  // the staging slot's previous DMA is done
+    const size_t sm_base = in_pinned ? o_m : 0;  // staged area starts at o_m when in_pinned
+    int32_t* hm = reinterpret_cast<int32_t*>(H + (o_m - sm_base));
+    int64_t* hoff = reinterpret_cast<int64_t*>(H + (o_off - sm_base));
+    std::memcpy(hm, b->m + c0, sizeof(int32_t) * cnt);
+    for (int64_t j = 0; j <= cnt; ++j) hoff[j] = b->offset[c0 + j] - e0;
+    const void* src[6] = {static_cast<const S*>(b->ax) + e0, static_cast<const S*>(b->ay) + e0,
+                          static_cast<const S*>(b->b) + e0,
+                          static_cast<const char*>(b->perm) + ps * e0,
+                          static_cast<const S*>(b->c) + 2 * c0,
+                          static_cast<const S*>(b->bound_m) + c0};
+    const size_t dst[6] = {o_ax, o_ay, o_b, o_perm, o_c, o_M};
+    const size_t len[6] = {sizeof(S) * E, sizeof(S) * E, sizeof(S) * E, ps * E,
+                           sizeof(S) * 2 * cnt, sizeof(S) * cnt};
+    for (int a = 0; a < 6; ++a) {
+      if (!len[a]) continue;
+      if (in_pinned) {
+        CUDA_TRY(cudaMemcpyAsync(D + dst[a], src[a], len[a], cudaMemcpyHostToDevice, cp));
+      } else {
+        std::memcpy(H + dst[a], src[a], len[a]);
+        CUDA_TRY(cudaMemcpyAsync(D + dst[a], H + dst[a], len[a], cudaMemcpyHostToDevice, cp));
+      }
+    }
+    CUDA_TRY(cudaMemcpyAsync(D + o_m, hm, (o_off - o_m) + sizeof(int64_t) * (cnt + 1),
+                             cudaMemcpyHostToDevice, cp));
+    CUDA_TRY(cudaEventRecord(hp.h2d[q], cp));
+    return 0;
+  };
+  // copy chunk k's results (slot k % 2) to the caller
+  auto gather = [&](int k) -> int {
+    const int q = k & 1;
+    const int64_t c0 = cut[k], cnt = cut[k + 1] - c0;
+    CUDA_TRY(cudaEventSynchronize(hp.d2h[q]));
+    const int64_t row0 = c0 / W, rows = out->iter_hist ? (cut[k + 1] - 1) / W - row0 + 1 : 0;
+    if (!out_pinned) {
+      const char* R = static_cast<const char*>(hp.pin_out[q]);
+      std::memcpy(out->status + c0, R + r_st, cnt);
+      std::memcpy(static_cast<T*>(out->x) + c0, R + r_x, sizeof(T) * cnt);
+      std::memcpy(static_cast<T*>(out->y) + c0, R + r_y, sizeof(T) * cnt);
+      std::memcpy(static_cast<T*>(out->value) + c0, R + r_v, sizeof(T) * cnt);
+      if (out->pair) std::memcpy(out->pair + 2 * c0, R + r_pair, sizeof(int32_t) * 2 * cnt);
+      if (out->violation_events)
+        std::memcpy(out->violation_events + c0, R + r_viol, sizeof(uint32_t) * cnt);
+      if (out->work_units) std::memcpy(out->work_units + c0, R + r_wu, sizeof(uint64_t) * cnt);
+    }
+    if (rows) {
+      // chunks and shards may share a block row: accumulate (zeroed by the caller)
+      const uint32_t* hsrc = out_pinned ? hist_host[q].data()
+                                        : reinterpret_cast<const uint32_t*>(
+                                              static_cast<const char*>(hp.pin_out[q]) + out_bytes);
+      static std::mutex hist_mu;
+      std::lock_guard<std::mutex> hl(hist_mu);
+      for (int64_t t = 0; t < rows * hstride; ++t) out->iter_hist[row0 * hstride + t] += hsrc[t];
+    }
+    return 0;
+  };
+
+  if (nk > 0)
+    if (int rc = upload(0)) return rc;
+  for (int k = 0; k < nk; ++k) {
+    const int q = k & 1;
+    if (k >= 1)
+      if (int rc = gather(k - 1)) return rc;  // frees staging slot (k+1) % 2
+    if (k + 1 < nk)
+      if (int rc = upload(k + 1)) return rc;  // behind chunk k-1's results on the copy stream
+    const int64_t c0 = cut[k], cnt = cut[k + 1] - c0;
+    const int64_t E = b->offset[cut[k + 1]] - b->offset[c0];
+    char* D = arena + q * slot_bytes;
+    char* R = D + in_bytes;
+    CUDA_TRY(cudaStreamWaitEvent(cs, hp.h2d[q], 0));
+    KParams kp = make_params<T>(o);
+    kp.n_list = cnt;
+    kp.list = nullptr;
+    kp.m = reinterpret_cast<const int32_t*>(D + o_m);
+    kp.offset = reinterpret_cast<const int64_t*>(D + o_off);
+    kp.ax = D + o_ax;
+    kp.ay = D + o_ay;
+    kp.b = D + o_b;
+    kp.perm = D + o_perm;
+    kp.c = D + o_c;
+    kp.bound_m = D + o_M;
+    kp.status = reinterpret_cast<uint8_t*>(R + r_st);
+    kp.x = R + r_x;
+    kp.y = R + r_y;
+    kp.value = R + r_v;
+    kp.pair = reinterpret_cast<int32_t*>(R + r_pair);
+    kp.viol = reinterpret_cast<uint32_t*>(R + r_viol);
+    kp.wu = reinterpret_cast<uint64_t*>(R + r_wu);
+    const int64_t row0 = c0 / W, rows = out->iter_hist ? (cut[k + 1] - 1) / W - row0 + 1 : 0;
+    if (rows) {
+      kp.iter_hist = reinterpret_cast<uint32_t*>(R + out_bytes);
+      kp.hist_lp0 = c0 - row0 * W;  // local LP 0 sits at this offset within row 0
+      kp.hist_w = (int32_t)W;
+      kp.hist_stride = (int32_t)hstride;
+      CUDA_TRY(cudaMemsetAsync(kp.iter_hist, 0, sizeof(uint32_t) * rows * hstride, cs));
+    }
+    if (int rc = solve_device_batch<S>(kp, E, min_m, max_m, b->perm_bits, o->scheduler, dev, cs, true))
+      return rc;
+    CUDA_TRY(cudaEventRecord(hp.solved[q], cs));
+    CUDA_TRY(cudaStreamWaitEvent(cp, hp.solved[q], 0));
+    // results: D2H on the copy stream (behind chunk k+1's inputs)
+    char* dstp = static_cast<char*>(hp.pin_out[q]);
+    auto d2h = [&](void* dst_user, size_t roff, size_t len) -> int {
+      if (!len) return 0;
+      void* dst = out_pinned ? dst_user : (void*)(dstp + roff);
+      CUDA_TRY(cudaMemcpyAsync(dst, R + roff, len, cudaMemcpyDeviceToHost, cp));
+      return 0;
+    };
+    int rc = d2h(out->status + c0, r_st, cnt);
+    if (!rc) rc = d2h(static_cast<T*>(out->x) + c0, r_x, sizeof(T) * cnt);
+    if (!rc) rc = d2h(static_cast<T*>(out->y) + c0, r_y, sizeof(T) * cnt);
+    if (!rc) rc = d2h(static_cast<T*>(out->value) + c0, r_v, sizeof(T) * cnt);
+    if (!rc && out->pair) rc = d2h(out->pair + 2 * c0, r_pair, sizeof(int32_t) * 2 * cnt);
+    if (!rc && out->violation_events)
+      rc = d2h(out->violation_events + c0, r_viol, sizeof(uint32_t) * cnt);
+    if (!rc && out->work_units) rc = d2h(out->work_units + c0, r_wu, sizeof(uint64_t) * cnt);
+    if (rc) return rc;
+    if (rows) {
+      void* hdst;
+      if (out_pinned) {
+        hist_host[q].assign((size_t)(rows * hstride), 0u);
+        hdst = hist_host[q].data();  // (pageable: this copy completes before returning)
+      } else {
+        hdst = dstp + out_bytes;
+      }
+      CUDA_TRY(cudaMemcpyAsync(hdst, kp.iter_hist, sizeof(uint32_t) * rows * hstride,
+                               cudaMemcpyDeviceToHost, cp));
+    }
+    CUDA_TRY(cudaEventRecord(hp.d2h[q], cp));
   }
-  if (int rc = solve_device_batch<S>(kp, E, min_m, max_m, b->perm_bits, o->scheduler, dev, s, true))
-    return rc;
-  std::vector<uint32_t> hist((size_t)(rows * hstride));
-  if (rows)
-    CUDA_TRY(cudaMemcpyAsync(hist.data(), kp.iter_hist, sizeof(uint32_t) * rows * hstride,
-                             cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(out->status + lo, A + off_st, cnt, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(static_cast<T*>(out->x) + lo, A + off_x, sizeof(T) * cnt,
-                           cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(static_cast<T*>(out->y) + lo, A + off_y, sizeof(T) * cnt,
-                           cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(static_cast<T*>(out->value) + lo, A + off_v, sizeof(T) * cnt,
-                           cudaMemcpyDeviceToHost, s));
-  if (out->pair)
-    CUDA_TRY(cudaMemcpyAsync(out->pair + 2 * lo, A + off_pair, sizeof(int32_t) * 2 * cnt,
-                             cudaMemcpyDeviceToHost, s));
-  if (out->violation_events)
-    CUDA_TRY(cudaMemcpyAsync(out->violation_events + lo, A + off_viol, sizeof(uint32_t) * cnt,
-                             cudaMemcpyDeviceToHost, s));
-  if (out->work_units)
-    CUDA_TRY(cudaMemcpyAsync(out->work_units + lo, A + off_wu, sizeof(uint64_t) * cnt,
-                             cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
-  if (rows) {
-    // shards may share a block row: accumulate (the caller's buffer was zeroed)
-    static std::mutex hist_mu;
-    std::lock_guard<std::mutex> lock(hist_mu);
-    for (int64_t q = 0; q < rows * hstride; ++q) out->iter_hist[row0 * hstride + q] += hist[q];
-  }
+  if (nk > 0)
+    if (int rc = gather(nk - 1)) return rc;
+  CUDA_TRY(cudaStreamSynchronize(cp));
+  CUDA_TRY(cudaStreamSynchronize(cs));
   return 0;
 }
 
@@ -929,8 +1116,12 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
   if (int rc = validate_common(b, o, out)) return rc;
   DeviceGuard guard;
   int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+  const int mock = b->mem == LP2D_MEM_HOST ? mock_devices() : 0;
+  if (mock) {
+    ndev = mock;  // test-only (see mock_devices): no CUDA, no solutions
+  } else if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     return fail(LP2D_ERR_CUDA, "no CUDA device visible (the solver has no CPU fallback)");
+  }
   if (b->mem == LP2D_MEM_DEVICE) {
     if (b->max_m < 0) return fail(LP2D_ERR_ARG, "device mode needs max_m");
     if (b->perm_bits == 16 && b->max_m > 65536)

@@ -18,3 +18,13 @@ def test_fp32_kernel_variant_parity(mode):
     r = subprocess.run([sys.executable, os.path.join(HERE, "variant_check.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("chunk", ["4096", "70000"])
+def test_host_mode_chunk_pipeline(chunk):
+    """Many chunks per shard (two device slots reused in turn, pinned and
+    pageable buffers, the lane_stats histogram accumulated over chunks)."""
+    env = dict(os.environ, LP2D_B200_CHUNK_ELEMS=chunk)
+    r = subprocess.run([sys.executable, os.path.join(HERE, "chunk_check.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
