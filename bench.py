@@ -521,6 +521,21 @@ def main():
     barrier()
     e2e_s = max_over_ranks(te1 - te0)
     e2e_value = world * pb.n * e2e_steps / e2e_s
+    # the same through the C ABI with the permutations generated on the
+    # device from the generator's seeds (lp2d_batch_soa::perm_from_seed):
+    # no permutation bytes cross PCIe
+    first = rank * n
+    hp_np = P.PackedBatch(hp.m, hp.offset, hp.ax, hp.ay, hp.b, None, hp.c, hp.M)
+    ps = P.PermSeed(seed, 2, 1, first)
+    P.solve_packed(hp_np, cfgb, out=hout, perm_seed=ps)
+    barrier()
+    te0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        P.solve_packed(hp_np, cfgb, out=hout, perm_seed=ps)
+    te1 = time.perf_counter()
+    barrier()
+    e2e_ps_value = world * pb.n * e2e_steps / max_over_ranks(te1 - te0)
+    h2d_ps = h2d - hp.perm.nbytes
 
     # ---- rank-0 extras: parity spot check, cpu baseline, JSON line ------------
     if rank == 0:
@@ -545,6 +560,11 @@ def main():
             "e2e": {"value": e2e_value, "unit": "LPs/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                     "lps_per_step": int(world * pb.n)},
+            "e2e_perm_seed": {"value": e2e_ps_value, "unit": "LPs/s",
+                              "h2d_bytes_per_step": int(h2d_ps), "d2h_bytes_per_step": int(d2h),
+                              "note": "e2e with the permutations generated on the device from "
+                                      "seeds (perm_from_seed): %d permutation bytes per step "
+                                      "not sent" % int(hp.perm.nbytes)},
             "gpu_launches": launches_p,
             "pipeline": {"streams": ns, "ms_per_step": ms_per_step,
                          "single_stream_ms_per_step": single_ms_per_step,

@@ -93,6 +93,20 @@ typedef struct lp2d_batch_soa {
   const void* bound_m; /* [n] */
   int64_t max_m;
   int64_t min_m;
+  /* Permutations from seeds (perm_from_seed != 0): LP j's insertion order is
+   * shuffle(m[j], derive_seed(perm_seed, perm_mul * (perm_first + j) +
+   * perm_add)) (serial.hpp:138-146 with rng.hpp:64-68), generated on the
+   * device instead of copied in: (mul, add) = (2, 1) are gen_mixed's /
+   * verify's streams (generate.hpp:186, bench.hpp:312), (1, 0) replicate's
+   * (generate.hpp:165-166). Host mode: perm may be NULL (nothing is read);
+   * device mode: perm is a device buffer the library fills (offset[n]
+   * entries of perm_bits). Zero-initialised callers keep explicit perms. */
+  int32_t perm_from_seed;
+  int32_t perm_mul;
+  int32_t perm_add;
+  int32_t _pad;
+  uint64_t perm_seed;
+  int64_t perm_first;
 } lp2d_batch_soa;
 
 /* block_config (batch.hpp:50-58) + tolerance (core.hpp:59-68). */

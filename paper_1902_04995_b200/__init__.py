@@ -7,6 +7,7 @@ from .lp2d import (  # noqa: F401
     Batch, BatchResult, BlockConfig, DeviceBatch, GenKind, PackedBatch, PackedResult,
     Permutation, Problem, SchedulerKind, Solution, Tolerance, derive_seed, gen, gen_mixed,
     identity_permutation, kernel_launches, lane_imbalance, replicate, shuffle, solve_batch, solve_device,
+    PermSeed,
     solve_packed,
 )
 from .lp2d import ParseError, problem_from_text, to_text  # noqa: F401  (io.hpp)

@@ -51,6 +51,12 @@ class BatchSoA(C.Structure):
         ("bound_m", C.c_void_p),
         ("max_m", C.c_int64),
         ("min_m", C.c_int64),
+        ("perm_from_seed", C.c_int32),
+        ("perm_mul", C.c_int32),
+        ("perm_add", C.c_int32),
+        ("_pad", C.c_int32),
+        ("perm_seed", C.c_uint64),
+        ("perm_first", C.c_int64),
     ]
 
 

@@ -686,8 +686,11 @@ int validate_common(const lp2d_batch_soa* b, const lp2d_opts* o, const lp2d_out*
     return fail(LP2D_ERR_ARG, "mem must be LP2D_MEM_HOST or LP2D_MEM_DEVICE");
   if (o->scheduler != LP2D_SCHED_NAIVE && o->scheduler != LP2D_SCHED_BALANCED)
     return fail(LP2D_ERR_ARG, "unknown scheduler");
-  if (!b->m || !b->offset || !b->ax || !b->ay || !b->b || !b->perm || !b->c || !b->bound_m)
+  if (!b->m || !b->offset || !b->ax || !b->ay || !b->b || !b->c || !b->bound_m)
     return fail(LP2D_ERR_ARG, "null batch array");
+  if (!b->perm && !(b->perm_from_seed && b->mem == LP2D_MEM_HOST))
+    return fail(LP2D_ERR_ARG, b->perm_from_seed ? "device mode: perm_from_seed needs the perm buffer to fill"
+                                                : "null batch array");
   if (!out->status || !out->x || !out->y || !out->value)
     return fail(LP2D_ERR_ARG, "null output array");
   return 0;
@@ -804,6 +807,35 @@ int solve_device_batch(KParams kp, int64_t E, int64_t min_m, int64_t max_m, int 
   } else {
     return launch_solve<double>(kp, min_m, max_m, perm_bits, sched, dev, s, may_sync);
   }
+}
+
+// Permutations of LPs [0, n) of a (sub)batch from seeds, global index
+// first + j (k_shuffle_seeded), into perm (device), on stream s.
+int shuffle_seeded(int64_t n, const int32_t* m, const int64_t* offset, int64_t max_m,
+                   uint64_t seed, int64_t first, int32_t mul, int32_t add, void* perm,
+                   int32_t perm_bits, cudaStream_t s) {
+  if (n <= 0) return 0;
+  const size_t es = perm_bits / 8;
+  int32_t ps = (int32_t)(((std::max<int64_t>(max_m, 1) + 7) / 8) * 8);
+  int threads = (int)std::min<int64_t>(128, (int64_t)(200 * 1024 / (ps * es)) & ~int64_t(31));
+  if (threads < 32) {  // large LPs: in place in global memory
+    ps = 0;
+    threads = 128;
+  }
+  const size_t smem = (size_t)threads * ps * es;
+  const unsigned grid = (unsigned)((n + threads - 1) / threads);
+  if (perm_bits == 16) {
+    auto k = k_shuffle_seeded<uint16_t>;
+    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, threads, smem, s>>>(n, m, offset, seed, first, mul, add, static_cast<uint16_t*>(perm), ps);
+  } else {
+    auto k = k_shuffle_seeded<uint32_t>;
+    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, threads, smem, s>>>(n, m, offset, seed, first, mul, add, static_cast<uint32_t*>(perm), ps);
+  }
+  note_launch();
+  CUDA_TRY(cudaGetLastError());
+  return 0;
 }
 
 // ---- host mode: one shard [lo, hi) on one device ----------------------------
@@ -955,7 +987,8 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     d.arena_bytes = 2 * slot_bytes;
   }
   const bool in_pinned = host_pinned(b->ax) && host_pinned(b->ay) && host_pinned(b->b) &&
-                         host_pinned(b->perm) && host_pinned(b->c) && host_pinned(b->bound_m);
+                         (b->perm_from_seed || host_pinned(b->perm)) && host_pinned(b->c) &&
+                         host_pinned(b->bound_m);
   const bool out_pinned = host_pinned(out->status) && host_pinned(out->x) && host_pinned(out->y) &&
                           host_pinned(out->value) && host_pinned(out->pair) &&
                           host_pinned(out->violation_events) && host_pinned(out->work_units);
@@ -982,14 +1015,14 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     for (int64_t j = 0; j <= cnt; ++j) hoff[j] = b->offset[c0 + j] - e0;
     const void* src[6] = {static_cast<const S*>(b->ax) + e0, static_cast<const S*>(b->ay) + e0,
                           static_cast<const S*>(b->b) + e0,
-                          static_cast<const char*>(b->perm) + ps * e0,
+                          b->perm ? static_cast<const char*>(b->perm) + ps * e0 : nullptr,
                           static_cast<const S*>(b->c) + 2 * c0,
                           static_cast<const S*>(b->bound_m) + c0};
     const size_t dst[6] = {o_ax, o_ay, o_b, o_perm, o_c, o_M};
     const size_t len[6] = {sizeof(S) * E, sizeof(S) * E, sizeof(S) * E, ps * E,
                            sizeof(S) * 2 * cnt, sizeof(S) * cnt};
     for (int a = 0; a < 6; ++a) {
-      if (!len[a]) continue;
+      if (!len[a] || (a == 3 && b->perm_from_seed)) continue;  // (perms generated on the device)
       if (in_pinned) {
         CUDA_TRY(cudaMemcpyAsync(D + dst[a], src[a], len[a], cudaMemcpyHostToDevice, cp));
       } else {
@@ -1044,6 +1077,12 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     char* D = arena + q * slot_bytes;
     char* R = D + in_bytes;
     CUDA_TRY(cudaStreamWaitEvent(cs, hp.h2d[q], 0));
+    if (b->perm_from_seed)
+      if (int rc = shuffle_seeded(cnt, reinterpret_cast<const int32_t*>(D + o_m),
+                                  reinterpret_cast<const int64_t*>(D + o_off), max_m, b->perm_seed,
+                                  b->perm_first + c0, b->perm_mul, b->perm_add, D + o_perm,
+                                  b->perm_bits, cs))
+        return rc;
     KParams kp = make_params<T>(o);
     kp.n_list = cnt;
     kp.list = nullptr;
@@ -1157,6 +1196,11 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
       kp.hist_w = (int32_t)W;
       kp.hist_stride = (int32_t)(b->max_m + 1);
     }
+    if (b->perm_from_seed)
+      if (int rc = shuffle_seeded(b->n, b->m, b->offset, b->max_m, b->perm_seed, b->perm_first,
+                                  b->perm_mul, b->perm_add, const_cast<void*>(b->perm), b->perm_bits,
+                                  static_cast<cudaStream_t>(o->stream)))
+        return rc;
     int64_t E = 0;  // scalar elements (offset[n]), needed to widen fp32 storage
     if constexpr (sizeof(S) == 4) {
       CUDA_TRY(cudaMemcpy(&E, b->offset + b->n, sizeof(int64_t), cudaMemcpyDeviceToHost));

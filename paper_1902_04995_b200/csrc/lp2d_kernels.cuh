@@ -1444,6 +1444,41 @@ __global__ void k_shuffle(int64_t n, const int32_t* m, const int64_t* offset,
   }
 }
 
+// Permutations from seeds inside a solve (lp2d_batch_soa::perm_from_seed):
+// LP j's order is shuffle(m[j], derive_seed(seed, mul * (first + j) + add))
+// (serial.hpp:138-146, rng.hpp:64-68; integer-only, so bit-identical to the
+// host). One thread per LP; the array is built in the thread's shared-memory
+// slice (ps entries, ps >= m) and streamed out in 16-byte vectors (segments
+// are 8-element aligned and padded, the layout contract); LPs larger than ps
+// shuffle in place in global memory.
+__device__ __forceinline__ uint64_t derive_seed_dev(uint64_t base, uint64_t stream);
+
+template <typename P>
+__global__ void k_shuffle_seeded(int64_t n, const int32_t* m, const int64_t* offset, uint64_t seed,
+                                 int64_t first, int32_t mul, int32_t add, P* perm, int32_t ps) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int32_t mj = m[j];
+  P* g = perm + offset[j];
+  Xoshiro r(derive_seed_dev(seed, (uint64_t)((int64_t)mul * (first + j) + add)));
+  const bool in_smem = mj <= ps;
+  P* o = in_smem ? reinterpret_cast<P*>(smem) + (size_t)threadIdx.x * ps : g;
+  for (int32_t i = 0; i < mj; ++i) o[i] = (P)i;
+  for (int64_t i = mj; i > 1; --i) {
+    const uint64_t q = r.below((uint64_t)i);
+    const P tmp = o[i - 1];
+    o[i - 1] = o[q];
+    o[q] = tmp;
+  }
+  if (in_smem) {
+    constexpr int V = 16 / (int)sizeof(P);
+    const uint4* src = reinterpret_cast<const uint4*>(o);
+    uint4* dst = reinterpret_cast<uint4*>(g);
+    for (int32_t v = 0; v < (mj + V - 1) / V; ++v) dst[v] = src[v];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Device-side instance synthesis: generate.hpp:60-91
 // (feasible_random, infeasible) plus the builder's unbounded kind, LP j of

@@ -367,25 +367,51 @@ def _opts(cfg: BlockConfig, tol: Tolerance, device: int = 0, stream: int = 0) ->
     return o
 
 
+@dataclass(frozen=True)
+class PermSeed:
+    """Permutations generated on the device (lp2d_batch_soa::perm_from_seed):
+    LP j's order is shuffle(m[j], derive_seed(seed, mul * (first + j) + add)).
+    mul=2, add=1: gen_mixed / PackedBatch.generate streams (generate.hpp:186);
+    mul=1, add=0: replicate's (generate.hpp:165-166)."""
+    seed: int
+    mul: int = 2
+    add: int = 1
+    first: int = 0
+
+
 def solve_packed(pb: PackedBatch, cfg: BlockConfig = BlockConfig(), tol: Tolerance = Tolerance(),
                  out: Optional[PackedResult] = None,
-                 iter_hist: Optional[np.ndarray] = None) -> PackedResult:
-    """Host-buffer solve through the C ABI (copies in/out inside the call)."""
+                 iter_hist: Optional[np.ndarray] = None,
+                 perm_seed: Optional[PermSeed] = None) -> PackedResult:
+    """Host-buffer solve through the C ABI (copies in/out inside the call).
+    With perm_seed, pb.perm is ignored (may be None): the permutations are
+    generated on the device and never cross PCIe."""
     if pb.n == 0:
         raise ValueError("solve_batch: empty batch")
     dt = pb.dtype
     if dt not in (np.float32, np.float64):
         raise ValueError("scalars must be float32 or float64")
-    arrs = [np.ascontiguousarray(a) for a in (pb.m, pb.offset, pb.ax, pb.ay, pb.b, pb.perm, pb.c, pb.M)]
+    perm_in = pb.perm if pb.perm is not None else np.zeros(0, np.uint16)
+    arrs = [np.ascontiguousarray(a) for a in (pb.m, pb.offset, pb.ax, pb.ay, pb.b, perm_in, pb.c, pb.M)]
     m, off, ax, ay, b, perm, c, M = arrs
+    if perm_seed is None and pb.perm is None:
+        raise ValueError("solve_batch: permutations missing (pass perm or perm_seed)")
     if out is None:
         # results are the reference's doubles for both storage types
         out = PackedResult(np.zeros(pb.n, np.uint8), np.zeros(pb.n), np.zeros(pb.n),
                            np.zeros(pb.n), np.zeros((pb.n, 2), np.int32),
                            np.zeros(pb.n, np.uint32), np.zeros(pb.n, np.uint64))
+    pbits = 16 if perm.dtype == np.uint16 else 32
+    if perm_seed is not None:
+        pbits = 16 if int(pb.m.max(initial=0)) <= 65536 else 32
     s = N.BatchSoA(pb.n, m.ctypes.data, off.ctypes.data, ax.ctypes.data, ay.ctypes.data,
-                   b.ctypes.data, perm.ctypes.data, 16 if perm.dtype == np.uint16 else 32,
+                   b.ctypes.data, perm.ctypes.data if perm_seed is None else None, pbits,
                    N.MEM_HOST, c.ctypes.data, M.ctypes.data, 0, 0)
+    if perm_seed is not None:
+        s.perm_from_seed = 1
+        s.perm_mul, s.perm_add = int(perm_seed.mul), int(perm_seed.add)
+        s.perm_seed = perm_seed.seed & (2**64 - 1)
+        s.perm_first = int(perm_seed.first)
     o = _opts(cfg, tol)
     r = N.Out(out.status.ctypes.data, out.x.ctypes.data, out.y.ctypes.data, out.value.ctypes.data,
               out.pair.ctypes.data, out.violation_events.ctypes.data, out.work_units.ctypes.data,

@@ -43,6 +43,10 @@ def main():
         h1 = np.zeros(rows * (int(sizes.max()) + 1), np.uint32)
         r1 = P.solve_packed(pb, P.BlockConfig(block_width=W), iter_hist=h1)
         check(r1, o, f"pageable {dt.__name__}")
+        # permutations generated on the device from the generator's seeds
+        noperm = P.PackedBatch(pb.m, pb.offset, pb.ax, pb.ay, pb.b, None, pb.c, pb.M)
+        r3 = P.solve_packed(noperm, P.BlockConfig(block_width=W), perm_seed=P.PermSeed(9))
+        check(r3, o, f"perm_seed {dt.__name__}")
         pp = P.PackedBatch(*(pinned(a) for a in (pb.m, pb.offset, pb.ax, pb.ay, pb.b, pb.perm,
                                                   pb.c, pb.M)))
         out = P.PackedResult(*(pinned(np.zeros(sh, d)) for sh, d in (

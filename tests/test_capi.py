@@ -89,3 +89,12 @@ def test_no_cpu_fallback(P):
     pb = P.PackedBatch.generate(np.full(4, 16, np.int32), 3)
     with pytest.raises(RuntimeError, match="no CUDA device"):
         P.solve_packed(pb)
+
+
+def test_perm_seed_api_validation(P):
+    pb = P.PackedBatch.generate(np.array([5, 6], np.int32), 1)
+    noperm = P.PackedBatch(pb.m, pb.offset, pb.ax, pb.ay, pb.b, None, pb.c, pb.M)
+    with pytest.raises(ValueError):
+        P.solve_packed(noperm)  # neither perm nor perm_seed
+    f = {n for n, _ in P.lp2d.N.BatchSoA._fields_}
+    assert {"perm_from_seed", "perm_mul", "perm_add", "perm_seed", "perm_first"} <= f

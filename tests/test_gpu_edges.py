@@ -129,3 +129,36 @@ def test_against_the_reference_bruteforce_oracle(P, O):
         assert feas == bf_feas, j
         if feas:
             assert P.lp2d.agree_sig_figs(float(r.value[j]), bf_value, 5), (j, r.value[j], bf_value)
+
+
+def test_perm_seed_device_mode_fills_the_generator_permutations(P):
+    """Device mode with perm_from_seed: the library writes shuffle(m,
+    derive_seed(seed, 2g+1)) for global LP g = first + j into the caller's
+    buffer (the PackedBatch generator's streams), then solves."""
+    import torch
+
+    sizes = np.array([0, 1, 7, 64, 300, 1024, 5000, 70000], np.int32)
+    pb = P.PackedBatch.generate(sizes, 17, first=1000, perm_bits=32)
+    db = P.DeviceBatch(pb)
+    db.perm.zero_()
+    out = db.empty_result()
+    s = P.lp2d.N.BatchSoA(db.n, db.m.data_ptr(), db.offset.data_ptr(), db.ax.data_ptr(),
+                          db.ay.data_ptr(), db.b.data_ptr(), db.perm.data_ptr(), 32,
+                          P.lp2d.N.MEM_DEVICE, db.c.data_ptr(), db.M.data_ptr(), db.max_m, db.min_m)
+    s.perm_from_seed, s.perm_mul, s.perm_add, s.perm_seed, s.perm_first = 1, 2, 1, 17, 1000
+    o = P.lp2d._opts(P.BlockConfig(), P.Tolerance(), device=0,
+                     stream=torch.cuda.current_stream().cuda_stream)
+    r = P.lp2d.N.Out(out.status.data_ptr(), out.x.data_ptr(), out.y.data_ptr(),
+                     out.value.data_ptr(), out.pair.data_ptr(), out.violation_events.data_ptr(),
+                     out.work_units.data_ptr())
+    import ctypes as C
+
+    assert P.lp2d.N.lib().lp2dgpu_solve_f64(C.byref(s), C.byref(o), C.byref(r)) == 0
+    torch.cuda.synchronize()
+    got = db.perm.cpu().numpy().view(np.uint32)
+    for j in range(pb.n):
+        a, b = int(pb.offset[j]), int(pb.offset[j]) + int(sizes[j])
+        assert np.array_equal(got[a:b], pb.perm[a:b]), j
+    ref = P.solve_packed(pb)
+    assert np.array_equal(out.status.cpu().numpy(), ref.status)
+    assert np.array_equal(out.x.cpu().numpy(), ref.x)
