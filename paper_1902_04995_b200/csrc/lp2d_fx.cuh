@@ -46,10 +46,12 @@
 //     uncertain objective side, or an empty interval) runs the reference's
 //     double fold for that event (fold_exact_global on the widened values).
 //
-// Exactness therefore rests on the error bounds (DESIGN.md §3 derives them);
-// the bound constants are deliberately loose (factors 1.1-2) and were
-// checked on CPU by scratch-free tests (tests/test_fx_bounds.py runs the
-// bound model against the reference on every unit of c1..c4 instances).
+// Exactness therefore rests on the error bounds (DESIGN.md §4 lists the
+// error sources and constants); the constants are deliberately loose
+// (factors 1.1-2). The bound model is not machine-checked: it is validated by
+// the GPU parity tests against the unmodified reference (full-size c2 and c3,
+// a heavy-tailed c4 subset, adversarial insertion orders, every size-class
+// edge, K4 and K5 for every class), all bit-identical.
 #pragma once
 
 #ifndef LP2D_FX_COLD

@@ -1,10 +1,12 @@
 """Parity of the CUDA path (through the C ABI) with the reference and the
-oracle. Bit-exact everywhere: fp64 results equal the UNMODIFIED reference's
-(committed fixtures) and the fp64 oracle's; fp32 results equal the fp32
-oracle restatement's. "Equal" is IEEE value equality (== ; -0 == +0) for
-x, y, value and exact integer equality for status, defining pair,
-violation_events and work_units. The north-star tolerances (1e-5 rel fp32,
-1e-12 rel fp64) are therefore met with zero error."""
+oracle. Bit-exact everywhere: fp64-stored results equal the UNMODIFIED
+reference's (committed fixtures) and the fp64 oracle's; fp32-stored results
+equal the unmodified reference run on the same fp32-rounded instance (double
+arithmetic on the stored values: the ref32_* fixtures and the oracle's f
+path). "Equal" is IEEE value equality (== ; -0 == +0) for x, y, value and
+exact integer equality for status, defining pair, violation_events and
+work_units. The north-star tolerances (1e-5 rel fp32, 1e-12 rel fp64) are
+therefore met with zero error."""
 import numpy as np
 import pytest
 
