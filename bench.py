@@ -553,7 +553,8 @@ def main():
                 algo_bytes / 1e6, ">" if algo_bytes > 126e6 else "<"),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
-                         "traffic": None if full else load_traffic(cfg),
+                         "traffic": None if full else load_traffic(
+                             cfg if dt == CONFIGS[cfg][2] else "%s-%s" % (cfg, "f32" if dt == np.float32 else "f64")),
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": algo_bytes,
                          "kernel_ms": kern_ms_max},

@@ -44,7 +44,11 @@ int fail(int code, const std::string& msg) {
 std::atomic<uint64_t> g_launches{0};
 inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-constexpr int kCounterSlots = 4096;
+// Ticket counter pairs, handed out round robin; a kernel leaves its pair at
+// zero when its last warp finishes. A pair is reused after kCounterSlots
+// launches on the device, so two launches could only share one if 2^16
+// launches were in flight at once (each solve issues at most ~16).
+constexpr int kCounterSlots = 1 << 16;
 
 // Per-device state: ticket counters (self-resetting, round-robin slots) and a
 // grow-only scratch arena for host-mode calls.
@@ -230,7 +234,7 @@ bool tiny_uses_lanes() {
 template <typename T, typename P, int MAXM = kLaneMaxM, typename S = T>
 int launch_lane_kernel(KParams kp, int dev, cudaStream_t stream) {
   auto kern = k_solve_lanes<T, P, MAXM, S>;
-  constexpr size_t smem = LaneTile<T, MAXM>::kSmem;
+  constexpr size_t smem = LaneTile<S, MAXM>::kSmem;
   static int blocks_per_sm[64] = {0};
   static std::mutex mu;  // concurrent first use from multi-GPU host threads
   std::lock_guard<std::mutex> lock(mu);
@@ -816,7 +820,9 @@ int shuffle_seeded(int64_t n, const int32_t* m, const int64_t* offset, int64_t m
                    int32_t perm_bits, cudaStream_t s) {
   if (n <= 0) return 0;
   const size_t es = perm_bits / 8;
-  int32_t ps = (int32_t)(((std::max<int64_t>(max_m, 1) + 7) / 8) * 8);
+  // shared-memory slices of up to 1024 entries (LPs above shuffle in global
+  // memory), so a few large LPs do not push a mixed batch out of smem
+  int32_t ps = (int32_t)(((std::min<int64_t>(std::max<int64_t>(max_m, 1), 1024) + 7) / 8) * 8);
   int threads = (int)std::min<int64_t>(128, (int64_t)(200 * 1024 / (ps * es)) & ~int64_t(31));
   if (threads < 32) {  // large LPs: in place in global memory
     ps = 0;

@@ -714,12 +714,14 @@ __device__ __forceinline__ Line<T> shfl_line(const Line<T>& l, int src) {
 template <typename T, typename P, int MAXM, typename S = T>
 __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid_constant__ KParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  using LT = LaneTile<T, MAXM>;
+  // the tile holds the STORED scalars (float storage: half the shared memory
+  // of a double tile, so twice the resident warps); reads widen exactly
+  using LT = LaneTile<S, MAXM>;
   constexpr int ST = LT::kStride;
   const int lane = threadIdx.x & 31, wic = threadIdx.x >> 5;
-  T* sx = reinterpret_cast<T*>(smem + wic * LT::kWarpBytes);
-  T* sy = sx + MAXM * ST;
-  T* sb = sy + MAXM * ST;
+  S* sx = reinterpret_cast<S*>(smem + wic * LT::kWarpBytes);
+  S* sy = sx + MAXM * ST;
+  S* sb = sy + MAXM * ST;
   // user constraint at considered position k (>= 4) of lane c's LP
   auto at = [&](int k, int c) { return (k - 4) * ST + c; };
   const int32_t* list;
@@ -799,9 +801,9 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
         const int k = k0 + u;
         if (k < MAXM && k < mj) {
           sbits = max(sbits, float_bits(fabs(vx[u]) + fabs(vy[u])));
-          sx[at(4 + k, lane)] = vx[u];
-          sy[at(4 + k, lane)] = vy[u];
-          sb[at(4 + k, lane)] = vb[u];
+          sx[at(4 + k, lane)] = (S)vx[u];
+          sy[at(4 + k, lane)] = (S)vy[u];
+          sb[at(4 + k, lane)] = (S)vb[u];
         }
       }
     }
@@ -823,7 +825,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
     // ---- lockstep sweep (serial.hpp:168-186 per lane) ----------------------
     for (int i = 4; i < pend; ++i) {
       const bool v = alive && i < mpos &&
-                     !satisfied(sx[at(i, lane)], sy[at(i, lane)], sb[at(i, lane)], St.px, St.py,
+                     !satisfied((T)sx[at(i, lane)], (T)sy[at(i, lane)], (T)sb[at(i, lane)], St.px, St.py,
                                 eps_feas);
       uint32_t vm = __ballot_sync(kFull, v);
       if (!vm) continue;
@@ -832,7 +834,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
         St.viol += 1;
         St.wu += (uint32_t)i;
         note_event(p, h.lp, (uint32_t)i);
-        l = boundary_of(sx[at(i, lane)], sy[at(i, lane)], sb[at(i, lane)]);
+        l = boundary_of((T)sx[at(i, lane)], (T)sy[at(i, lane)], (T)sb[at(i, lane)]);
       }
       const int nv = __popc(vm);
       if (nv * (((i + 31) >> 5) * 26 + 64) >= i * 22) {
@@ -851,7 +853,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
           }
 #pragma unroll 4
           for (int k = 4; k < i; ++k)
-            wu_fold(sx[at(k, lane)], sy[at(k, lane)], sb[at(k, lane)], l, lpbnd, (uint32_t)k,
+            wu_fold((T)sx[at(k, lane)], (T)sy[at(k, lane)], (T)sb[at(k, lane)], l, lpbnd, (uint32_t)k,
                     true, acc, rare);
           if (rare) {  // exact reference fold for this lane (rare)
             acc.uL = -T(INFINITY);
@@ -863,7 +865,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
               wu_apply(bx, by, bb, l, eps_par, eps_feas, eps_hi, (uint32_t)k, acc);
             }
             for (int k = 4; k < i; ++k)
-              wu_apply(sx[at(k, lane)], sy[at(k, lane)], sb[at(k, lane)], l, eps_par, eps_feas,
+              wu_apply((T)sx[at(k, lane)], (T)sy[at(k, lane)], (T)sb[at(k, lane)], l, eps_par, eps_feas,
                        eps_hi, (uint32_t)k, acc);
           }
           Merged<T> mg;
@@ -892,9 +894,9 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
             if (k < 4) {
               box_unit(k, Mc, x, y, bb);
             } else {
-              x = sx[at(k, c)];
-              y = sy[at(k, c)];
-              bb = sb[at(k, c)];
+              x = (T)sx[at(k, c)];
+              y = (T)sy[at(k, c)];
+              bb = (T)sb[at(k, c)];
             }
             wu_fold(x, y, bb, lc, bnd, (uint32_t)k, true, acc, rare);
           }
@@ -908,9 +910,9 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
               if (k < 4) {
                 box_unit(k, Mc, x, y, bb);
               } else {
-                x = sx[at(k, c)];
-                y = sy[at(k, c)];
-                bb = sb[at(k, c)];
+                x = (T)sx[at(k, c)];
+                y = (T)sy[at(k, c)];
+                bb = (T)sb[at(k, c)];
               }
               wu_apply(x, y, bb, lc, eps_par, eps_feas, eps_hi, (uint32_t)k, acc);
             }
