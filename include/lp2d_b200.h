@@ -148,7 +148,7 @@ void lp2dgpu_default_opts(lp2d_opts* opts);
 
 /* Solve a batch. Host mode: shards the batch over n_gpus devices (LP ranges
  * balanced by sum(m + 4), one host thread per device); each shard is cut into
- * chunks (LP2D_B200_CHUNK_ELEMS elements, default 16 Mi) pipelined over two
+ * chunks (LP2D_B200_CHUNK_ELEMS elements, default 4 Mi) pipelined over two
  * device slots (H2D of the next chunk overlaps the solve of the current one;
  * pageable inputs are staged through pinned buffers, pinned ones are DMA'd
  * directly); returns when every result is in place. Device mode: enqueues on

@@ -830,15 +830,18 @@ int shuffle_seeded(int64_t n, const int32_t* m, const int64_t* offset, int64_t m
   }
   const size_t smem = (size_t)threads * ps * es;
   const unsigned grid = (unsigned)((n + threads - 1) / threads);
-  if (perm_bits == 16) {
-    auto k = k_shuffle_seeded<uint16_t>;
-    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, threads, smem, s>>>(n, m, offset, seed, first, mul, add, static_cast<uint16_t*>(perm), ps);
-  } else {
-    auto k = k_shuffle_seeded<uint32_t>;
-    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, threads, smem, s>>>(n, m, offset, seed, first, mul, add, static_cast<uint32_t*>(perm), ps);
-  }
+  // (the dynamic shared-memory opt-in, once per process and kernel: 200 KB)
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(k_shuffle_seeded<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_shuffle_seeded<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  });
+  if (perm_bits == 16)
+    k_shuffle_seeded<uint16_t><<<grid, threads, smem, s>>>(n, m, offset, seed, first, mul, add,
+                                                           static_cast<uint16_t*>(perm), ps);
+  else
+    k_shuffle_seeded<uint32_t><<<grid, threads, smem, s>>>(n, m, offset, seed, first, mul, add,
+                                                           static_cast<uint32_t*>(perm), ps);
   note_launch();
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -858,7 +861,7 @@ int64_t chunk_elems() {
   static const int64_t v = [] {
     const char* e = std::getenv("LP2D_B200_CHUNK_ELEMS");
     const long long x = e ? std::atoll(e) : 0;
-    return x > 0 ? (int64_t)x : (int64_t)(16 << 20);
+    return x > 0 ? (int64_t)x : (int64_t)(4 << 20);
   }();
   return v;
 }
