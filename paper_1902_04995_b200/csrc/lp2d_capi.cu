@@ -123,7 +123,13 @@ static_assert(kLaneMaxM + 1 + kNumSlotClasses + 64 <= kMaxBins, "bins fit kMaxBi
 
 template <typename T>
 constexpr int max_nslot() {
-  return 129;  // warp classes up to m <= 4124 (larger LPs: the CTA kernel)
+  // warp classes up to m <= 2076; larger LPs: the CTA kernel (one LP per CTA,
+  // every thread of the CTA dealt its work units). Measured per uniform batch
+  // (B200, per 2^13 LPs / 2^12 at m = 4000): fp32 storage m = 2100 459 vs 520
+  // us, 3000 533 vs 577, 4000 339 vs 412; fp64 m = 2100 449 vs 688, 3000 859
+  // vs 886, 4000 505 vs 572; at m <= 2000 the warp classes win (m = 2000: 356
+  // vs 450 fp32, 366 vs 435 fp64).
+  return 65;
 }
 
 // Eps_par rounded up by 2^-10 (relative), in T: the parallel-filter factor.
@@ -327,7 +333,7 @@ int launch_cta_kernel(KParams kp, int64_t max_m, int dev, cudaStream_t stream) {
   const size_t smem = CtaBuffers<T, P, S>::bytes(cap);
   // 16 warps per SM, split over as many CTAs (LPs) as shared memory allows
   const int ctas = (int)std::max<size_t>(1, (size_t)per_sm / (smem + 1024));
-  if (ctas >= 4) return launch_cta_t<T, P, 128, S>(kp, cap, smem, dev, stream);
+  if (ctas >= 3) return launch_cta_t<T, P, 128, S>(kp, cap, smem, dev, stream);
   if (ctas >= 2) return launch_cta_t<T, P, 256, S>(kp, cap, smem, dev, stream);
   return launch_cta_t<T, P, 512, S>(kp, cap, smem, dev, stream);
 }
@@ -371,9 +377,6 @@ int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t ma
     case 65:  // 16 register chunks + 49 tail chunks (m <= 2076, 29 KB per warp; fp64 2 + 63)
       if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 63>(kp, dev, s, max_m);
       else return launch_warp_kernel<T, P, 16, 49>(kp, dev, s, max_m);
-    case 129:
-      if constexpr (sizeof(T) == 8) return launch_warp_kernel<T, P, 2, 127>(kp, dev, s, max_m);
-      else return launch_warp_kernel<T, P, 16, 113>(kp, dev, s, max_m);
   }
   return fail(LP2D_ERR_UNSUPPORTED, "size class not built");
 }
@@ -446,7 +449,7 @@ int launch_fx(KParams kp, int64_t max_m, int dev, cudaStream_t s) {
 #define LP2D_FX_NS33 8  // register chunks of the m <= 1052 class (config 2)
 #endif
 
-// K4/K5 cover the warp classes (29 <= m <= 4124); the lane class and the CTA
+// K4/K5 cover the warp classes (29 <= m <= 2076); the lane class and the CTA
 // class read the float storage directly (their kernels' S = float).
 bool fx_class(int cls) { return cls >= 1 && cls < n_reg_classes<double>(); }
 
@@ -534,7 +537,6 @@ int launch_fx_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t
     case 18: return launch_fx<P, 10, 8>(kp, max_m, dev, s);
     case 33: return launch_fx<P, LP2D_FX_NS33, 33 - LP2D_FX_NS33>(kp, max_m, dev, s);
     case 65: return launch_fx<P, 16, 49>(kp, max_m, dev, s);
-    case 129: return launch_fx<P, 16, 113>(kp, max_m, dev, s);
   }
   return fail(LP2D_ERR_UNSUPPORTED, "fx size class not built");
 }
@@ -785,6 +787,11 @@ int solve_f32_balanced(KParams kp, int64_t E, int64_t min_m, int64_t max_m, int 
   return launch_binned<double>(
       kp, min_m, max_m, dev, s, may_sync,
       [&](const KParams& kc, int c, int d, cudaStream_t cs, int64_t cap_m) {
+        // (experiment knob: LP2D_B200_FORCE_CTA=1 sends every class above the
+        // lane class to the CTA kernel)
+        static const bool force_cta = std::getenv("LP2D_B200_FORCE_CTA") &&
+                                      std::getenv("LP2D_B200_FORCE_CTA")[0] == '1';
+        if (force_cta && c >= 1) return launch_cta_kernel<double, P, float>(kc, cap_m, d, cs);
         if (fx_class(c)) return launch_fx_class<P>(kc, c, d, cs, cap_m);
         // the lane class (m <= 28) and the CTA class (large LPs) read the
         // float storage directly and widen on load (exact)
