@@ -837,12 +837,21 @@ int shuffle_seeded(int64_t n, const int32_t* m, const int64_t* offset, int64_t m
   }
   const size_t smem = (size_t)threads * ps * es;
   const unsigned grid = (unsigned)((n + threads - 1) / threads);
-  // (the dynamic shared-memory opt-in, once per process and kernel: 200 KB)
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(k_shuffle_seeded<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_shuffle_seeded<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  });
+  // (the dynamic shared-memory opt-in, once per device and kernel: 200 KB)
+  {
+    static bool done[64] = {};
+    static std::mutex mu;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+      CUDA_TRY(cudaFuncSetAttribute(k_shuffle_seeded<uint16_t>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      CUDA_TRY(cudaFuncSetAttribute(k_shuffle_seeded<uint32_t>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      done[dev] = true;
+    }
+  }
   if (perm_bits == 16)
     k_shuffle_seeded<uint16_t><<<grid, threads, smem, s>>>(n, m, offset, seed, first, mul, add,
                                                            static_cast<uint16_t*>(perm), ps);
