@@ -445,10 +445,6 @@ int launch_fx(KParams kp, int64_t max_m, int dev, cudaStream_t s) {
   return launch_fx_cap<P, NS, NT, 0>(kp, dev, s);
 }
 
-#ifndef LP2D_FX_NS33
-#define LP2D_FX_NS33 8  // register chunks of the m <= 1052 class (config 2)
-#endif
-
 // K4/K5 cover the warp classes (29 <= m <= 2076); the lane class and the CTA
 // class read the float storage directly (their kernels' S = float).
 bool fx_class(int cls) { return cls >= 1 && cls < n_reg_classes<double>(); }
@@ -496,7 +492,7 @@ int launch_fs(KParams kp, int dev, cudaStream_t stream) {
   return 0;
 }
 
-// 0: K4 only, 1: K5 for the classes where it is faster (default), 2: K5 for all.
+// 0 or 1: K4 (the default), 2 ("all"): K5 for every class <= 1052 (A/B).
 int fs_mode() {
   static const int mode = [] {
     const char* e = std::getenv("LP2D_B200_FS");
@@ -509,13 +505,12 @@ int fs_mode() {
 
 template <typename P>
 int launch_fx_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t max_m) {
-  // K5 where it measured faster than K4 (B200, per uniform batch; DESIGN.md
-  // §3): the 317 <= m <= 572 class (m = 500: 343 vs 439 us per 2^15 LPs).
-  // Below, K4's register-resident chunks win (m = 128: 664 vs 876 us per
-  // 2^17); at m = 1024 the two tie (277 vs 283 us per 2^14).
-  // LP2D_B200_FS=all routes every class <= 1052 to K5, =0 none (A/B knobs).
+  // K5 (insertion-order shared memory) for every class <= 1052 only on
+  // request (LP2D_B200_FS=all; the default and =0 run K4): K4 measured
+  // faster everywhere once its tail classes keep 2 register chunks (B200,
+  // m = 500: 293 vs 345 us per 2^15 LPs, m = 1024: 235 vs 283 per 2^14).
   const int fs = fs_mode();
-  if (fs == 2 || (fs == 1 && kSlotClasses[cls] == 18)) {
+  if (fs == 2) {
     switch (kSlotClasses[cls]) {
       case 2: return launch_fs<P, 60, 2, 20>(kp, dev, s);
       case 4: return launch_fs<P, 124, 2, 20>(kp, dev, s);
@@ -527,16 +522,22 @@ int launch_fx_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t
       case 33: return launch_fs<P, 1052, 1, 15>(kp, dev, s);
     }
   }
+  // Register-only classes up to m = 188; above, 2 register chunks + a
+  // shared-memory tail walked through the staged permutation. Measured per
+  // uniform batch (B200): m = 150 362 vs 406 us per 2^16 LPs (register-only
+  // wins), m = 250 526 vs 443, m = 300 545 vs 470, m = 1100 284 vs 211 per
+  // 2^13, m = 2000 360 vs 287 (2-chunk tails win: 8 or 16 register chunks
+  // hold more registers and code, and fewer warps hide the per-event latency).
   switch (kSlotClasses[cls]) {
     case 2: return launch_fx<P, 2, 0>(kp, max_m, dev, s);
     case 4: return launch_fx<P, 4, 0>(kp, max_m, dev, s);
     case 5: return launch_fx<P, 5, 0>(kp, max_m, dev, s);
     case 6: return launch_fx<P, 6, 0>(kp, max_m, dev, s);
-    case 9: return launch_fx<P, 9, 0>(kp, max_m, dev, s);
-    case 10: return launch_fx<P, 10, 0>(kp, max_m, dev, s);
-    case 18: return launch_fx<P, 10, 8>(kp, max_m, dev, s);
-    case 33: return launch_fx<P, LP2D_FX_NS33, 33 - LP2D_FX_NS33>(kp, max_m, dev, s);
-    case 65: return launch_fx<P, 16, 49>(kp, max_m, dev, s);
+    case 9: return launch_fx<P, 2, 7>(kp, max_m, dev, s);
+    case 10: return launch_fx<P, 2, 8>(kp, max_m, dev, s);
+    case 18: return launch_fx<P, 2, 16>(kp, max_m, dev, s);
+    case 33: return launch_fx<P, 2, 31>(kp, max_m, dev, s);
+    case 65: return launch_fx<P, 2, 63>(kp, max_m, dev, s);
   }
   return fail(LP2D_ERR_UNSUPPORTED, "fx size class not built");
 }
