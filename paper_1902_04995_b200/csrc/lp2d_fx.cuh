@@ -60,6 +60,19 @@
 
 namespace lp2d_b200 {
 
+#ifndef LP2D_FX_EXACT_BATCH
+#define LP2D_FX_EXACT_BATCH 1
+#endif
+#ifndef LP2D_FX_SHIFT_BATCH
+#define LP2D_FX_SHIFT_BATCH 2
+#endif
+// Loads in flight per lane in the exact fold and in a reshift's staged
+// rewrite. Small on purpose: these paths are inlined (calls measured slower)
+// and their unrolled bodies crowd the hot loops out of the instruction cache
+// (B200, 8 -> 1/2: c2 0.231 -> 0.219 ms, c3 0.809 -> 0.698 ms, c4 0.804 ->
+// 0.758 ms).
+constexpr int kFxExactBatch = LP2D_FX_EXACT_BATCH;
+constexpr int kFxShiftBatch = LP2D_FX_SHIFT_BATCH;
 constexpr float kU32 = 0x1p-24f;   // fp32 unit roundoff
 constexpr float kU64 = 0x1p-53f;   // fp64 unit roundoff (a normal float)
 constexpr float kRho = 0x1p-21f;   // MUFU rcp/rsqrt relative error bound (PTX: <= 1 ulp / 2^-22.9)
@@ -294,10 +307,10 @@ __device__ __forceinline__ Acc<double> fx_fold_exact(const KParams& p, int64_t o
   acc.uR = INFINITY;
   acc.oL = acc.oR = acc.par = kNone;
 #pragma unroll 1
-  for (uint32_t k0 = lane; k0 < pi; k0 += 32 * 8) {
-    float vx[8], vy[8], vb[8];
+  for (uint32_t k0 = lane; k0 < pi; k0 += 32 * kFxExactBatch) {
+    float vx[kFxExactBatch], vy[kFxExactBatch], vb[kFxExactBatch];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < kFxExactBatch; ++u) {
       const uint32_t k = k0 + 32 * u;
       const bool in = k < pi && k >= 4;
       const uint32_t o = in ? (sperm ? (uint32_t)sperm[k - 4] : (uint32_t)gp[k - 4]) : 0u;
@@ -306,7 +319,7 @@ __device__ __forceinline__ Acc<double> fx_fold_exact(const KParams& p, int64_t o
       vb[u] = in ? __ldg(gb + o) : 0.0f;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < kFxExactBatch; ++u) {
       const uint32_t k = k0 + 32 * u;
       if (k < pi) {
         double x = vx[u], y = vy[u], bb = vb[u];
@@ -596,15 +609,15 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
         float4* sb4 = reinterpret_cast<float4*>(sb);
         const float4* gb4 = reinterpret_cast<const float4*>(static_cast<const float*>(p.b) + h.off);
 #pragma unroll 1
-        for (int g0 = lane; g0 < nv; g0 += 32 * 8) {
-          float4 vb[8];
+        for (int g0 = lane; g0 < nv; g0 += 32 * kFxShiftBatch) {
+          float4 vb[kFxShiftBatch];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < kFxShiftBatch; ++u) {
             const int g = g0 + 32 * u;
             vb[u] = g < nv ? (shifted ? __ldg(gb4 + g) : sb4[g]) : make_float4(0, 0, 0, 0);
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < kFxShiftBatch; ++u) {
             const int g = g0 + 32 * u;
             if (g < nv) {
               const float4 vx = reinterpret_cast<const float4*>(sax)[g];

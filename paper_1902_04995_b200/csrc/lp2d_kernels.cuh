@@ -1458,7 +1458,7 @@ __device__ __forceinline__ uint64_t derive_seed_dev(uint64_t base, uint64_t stre
 template <typename P>
 __global__ void k_shuffle_seeded(int64_t n, const int32_t* m, const int64_t* offset, uint64_t seed,
                                  int64_t first, int32_t mul, int32_t add, P* perm, int32_t ps) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int32_t mj = m[j];
