@@ -389,10 +389,11 @@ int launch_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t ma
 // kernels (WarpLayout<float, ...>): register-only classes at a compile-time
 // CTA shape, late-TMA classes at the run-time shape with the most resident
 // warps.
-template <typename P, int NS, int NT, int CAP>
+template <typename P, int NS, int NT, int CAP, bool DB = false>
 int launch_fx_cap(KParams kp, int dev, cudaStream_t stream) {
   using L = WarpLayout<float, P, NS, NT, CAP>;
-  auto kern = k_solve_fx<P, NS, NT, CAP>;
+  auto kern = k_solve_fx<P, NS, NT, CAP, DB>;
+  constexpr size_t nbuf = DB ? 2 : 1;
   struct Shape {
     int warps = 0, blocks = 0;
   };
@@ -410,7 +411,7 @@ int launch_fx_cap(KParams kp, int dev, cudaStream_t stream) {
         for (int w = 1; w <= L::kMaxWarpsRt; ++w) {
           int b = 0;
           CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, w * 32,
-                                                                 (size_t)w * (L::kBuf + 8)));
+                                                                 (size_t)w * nbuf * (L::kBuf + 8)));
           if (b * w > best.blocks * best.warps) best = Shape{w, b};
         }
       } else {
@@ -425,7 +426,7 @@ int launch_fx_cap(KParams kp, int dev, cudaStream_t stream) {
     }
     sh = shape[dev];
   }
-  const size_t smem = L::kLateTma ? (size_t)sh.warps * (L::kBuf + 8) : (size_t)L::kSmem;
+  const size_t smem = L::kLateTma ? (size_t)sh.warps * nbuf * (L::kBuf + 8) : (size_t)L::kSmem;
   const int64_t want = (kp.n_list + sh.warps - 1) / sh.warps;
   const int64_t maxb = (int64_t)sh.blocks * g_dev[dev].sm_count;
   const int grid = (int)std::max<int64_t>(1, std::min(want, maxb));
@@ -437,12 +438,12 @@ int launch_fx_cap(KParams kp, int dev, cudaStream_t stream) {
   return 0;
 }
 
-template <typename P, int NS, int NT>
+template <typename P, int NS, int NT, bool DB = false>
 int launch_fx(KParams kp, int64_t max_m, int dev, cudaStream_t s) {
   if constexpr (NS + NT == 33) {
-    if (max_m > 0 && max_m <= 1024) return launch_fx_cap<P, NS, NT, 1024>(kp, dev, s);
+    if (max_m > 0 && max_m <= 1024) return launch_fx_cap<P, NS, NT, 1024, DB>(kp, dev, s);
   }
-  return launch_fx_cap<P, NS, NT, 0>(kp, dev, s);
+  return launch_fx_cap<P, NS, NT, 0, DB>(kp, dev, s);
 }
 
 // K4/K5 cover the warp classes (29 <= m <= 2076); the lane class and the CTA
@@ -522,17 +523,19 @@ int launch_fx_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t
       case 33: return launch_fs<P, 1052, 1, 15>(kp, dev, s);
     }
   }
-  // Register-only classes up to m = 188; above, 2 register chunks + a
-  // shared-memory tail walked through the staged permutation. Measured per
-  // uniform batch (B200): m = 150 362 vs 406 us per 2^16 LPs (register-only
-  // wins), m = 250 526 vs 443, m = 300 545 vs 470, m = 1100 284 vs 211 per
-  // 2^13, m = 2000 360 vs 287 (2-chunk tails win: 8 or 16 register chunks
-  // hold more registers and code, and fewer warps hide the per-event latency).
+  // Every class above m = 60 keeps 2 register chunks + a shared-memory tail
+  // walked through the staged permutation (more register chunks hold more
+  // registers and unrolled code: m = 1100 284 vs 211 us per 2^13 LPs with 16
+  // vs 2, c2 0.284 vs 0.228 ms with 8 vs 2). Up to m = 188 the tail classes
+  // are double-buffered (the next LP's bulk copy overlaps this LP: m = 64 584
+  // -> 515 us per 2^17, m = 100 339 -> 305 per 2^16, c3 0.705 -> 0.635 ms);
+  // above, one buffer and the late copy (m = 250: 375 vs 387 us per 2^16,
+  // m = 500: 264 vs 292 per 2^15: more resident warps win).
   switch (kSlotClasses[cls]) {
     case 2: return launch_fx<P, 2, 0>(kp, max_m, dev, s);
-    case 4: return launch_fx<P, 4, 0>(kp, max_m, dev, s);
-    case 5: return launch_fx<P, 5, 0>(kp, max_m, dev, s);
-    case 6: return launch_fx<P, 6, 0>(kp, max_m, dev, s);
+    case 4: return launch_fx<P, 2, 2, true>(kp, max_m, dev, s);
+    case 5: return launch_fx<P, 2, 3, true>(kp, max_m, dev, s);
+    case 6: return launch_fx<P, 2, 4, true>(kp, max_m, dev, s);
     case 9: return launch_fx<P, 2, 7>(kp, max_m, dev, s);
     case 10: return launch_fx<P, 2, 8>(kp, max_m, dev, s);
     case 18: return launch_fx<P, 2, 16>(kp, max_m, dev, s);

@@ -457,14 +457,20 @@ struct FxBounds {
   static constexpr int kMinBlocks = L::kLateTma ? L::kMinBlocksRt : (L::kMinBlocks < 3 ? L::kMinBlocks : 3);
 };
 
-template <typename P, int NS, int NT, int CAP = 0>
+// DB (tail classes): two staging buffers per warp — the next LP's bulk copy
+// is issued into the other buffer when an LP starts instead of when it ends,
+// so short LPs do not wait on it.
+template <typename P, int NS, int NT, int CAP = 0, bool DB = false>
 __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt * 32,
                                   (FxBounds<WarpLayout<float, P, NS, NT, CAP>>::kMinBlocks))
     k_solve_fx(const __grid_constant__ KParams p) {
   static_assert(NS >= 1 && NS <= 40, "slot count");
   static_assert(NT == 0 || NS % 2 == 0, "the tail starts at a pair boundary");
+  static_assert(!DB || NT > 0, "double buffering is for the tail classes");
   using T = float;
   using L = WarpLayout<float, P, NS, NT, CAP>;
+  constexpr bool LATE = L::kLateTma && !DB;  // next LP's TMA issued at the end of this one
+  constexpr int NBUF = DB ? 2 : 1;
   const int W = L::kLateTma ? (int)(blockDim.x >> 5) : L::kWarps;
   constexpr uint32_t cap = (uint32_t)L::kCap;
   constexpr uint32_t arr = L::kArr;
@@ -473,8 +479,12 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wic = threadIdx.x >> 5;
-  unsigned char* buf = smem + wic * bufb;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + W * bufb) + wic;
+  unsigned char* const buf0 = smem + (size_t)wic * NBUF * bufb;
+  uint64_t* const bar0 = reinterpret_cast<uint64_t*>(smem + (size_t)W * NBUF * bufb) + wic * NBUF;
+  int cur = 0;
+  uint32_t phases = 0;  // mbarrier parity per buffer (bit)
+  unsigned char* buf = buf0;
+  uint64_t* bar = bar0;
   const float* sax = reinterpret_cast<const float*>(buf);
   const float* say = reinterpret_cast<const float*>(buf + arr);
   float* sb = reinterpret_cast<float*>(buf + 2 * arr);  // b, after a reshift b' (frame s)
@@ -485,20 +495,19 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
   const PairConsts pk = p.pk;
   const uint64_t policy = policy_evict_first();
 
-  if (lane == 0) mbar_init(bar, 1);
+  if (lane < NBUF) mbar_init(bar0 + lane, 1);
   __syncwarp();
 
   const int32_t* list;
   int64_t n_list;
   resolve_list(p, list, n_list);
-  uint32_t phase = 0;
   const int64_t TW = p.total_warps;
   const int64_t j0 = (int64_t)blockIdx.x * W + wic;
   auto lp_of = [&](int64_t t) -> int64_t { return t < n_list ? (list ? (int64_t)list[t] : t) : -1; };
-  constexpr int64_t kAhead = L::kLateTma ? 1 : 2;
-  int64_t lpA = lp_of(j0), lpB = L::kLateTma ? -1 : lp_of(j0 + TW);
+  constexpr int64_t kAhead = LATE ? 1 : 2;
+  int64_t lpA = lp_of(j0), lpB = LATE ? -1 : lp_of(j0 + TW);
   uint32_t hA = load_header_word<T>(p, lpA, lane);
-  uint32_t hB = L::kLateTma ? 0u : load_header_word<T>(p, lpB, lane);
+  uint32_t hB = LATE ? 0u : load_header_word<T>(p, lpB, lane);
   uint32_t ticket = atomic_add_if(p.counter, lane == 0, p.pk.zero);
   Header<T> h = unpack_header<L, T>(hA, lpA);
   issue_tma_warp<L, T, P>(p, h, buf, bar, policy, arr, lane);
@@ -506,8 +515,16 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
   uint32_t pend_pos = kNone, pend_q = 0;
 
   while (h.lp >= 0) {
-    mbar_wait(bar, phase);
-    phase ^= 1u;
+    if constexpr (DB) {
+      buf = buf0 + cur * bufb;
+      bar = bar0 + cur;
+      sax = reinterpret_cast<const float*>(buf);
+      say = reinterpret_cast<const float*>(buf + arr);
+      sb = reinterpret_cast<float*>(buf + 2 * arr);
+      sperm = reinterpret_cast<const P*>(buf + 3 * arr);
+    }
+    mbar_wait(bar, (phases >> cur) & 1u);
+    phases ^= 1u << cur;
 #ifdef LP2D_FX_TIMELINE
     uint64_t tl0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl0));
@@ -579,14 +596,19 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
       fence_proxy_async_smem();
     }
     Header<T> hn;
-    if constexpr (!L::kLateTma) {
+    if constexpr (!LATE) {
+      // register-only classes: the buffer was consumed by the gather; DB: the
+      // other buffer's LP finished (and fenced) one LP ago
       hn = unpack_header<L, T>(hB, lpB);
-      issue_tma_warp<L, T, P>(p, hn, buf, bar, policy, arr, lane);
+      if constexpr (DB)
+        issue_tma_warp<L, T, P>(p, hn, buf0 + (cur ^ 1) * bufb, bar0 + (cur ^ 1), policy, arr, lane);
+      else
+        issue_tma_warp<L, T, P>(p, hn, buf, bar, policy, arr, lane);
     }
     const int64_t tk = (int64_t)__shfl_sync(kFull, ticket, 0) + kAhead * TW;
     lpB = lp_of(tk);
     hB = load_header_word<T>(p, lpB, lane);
-    if constexpr (!L::kLateTma) ticket = atomic_add_if(p.counter, lane == 0, p.pk.zero);
+    if constexpr (!LATE) ticket = atomic_add_if(p.counter, lane == 0, p.pk.zero);
 
     // ---- solve (serial.hpp:159-188) -----------------------------------------
     // range guard: outside it the fp32 filter has no proven bounds (and
@@ -963,10 +985,12 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
         p.pair[2 * h.lp + lane] = pair_code(pos, q);
       }
       __syncwarp();
-      fence_proxy_async_smem();
-      hn = unpack_header<L, T>(hB, lpB);
-      issue_tma_warp<L, T, P>(p, hn, buf, bar, policy, arr, lane);
-      ticket = atomic_add_if(p.counter, lane == 0, p.pk.zero);
+      fence_proxy_async_smem();  // (DB: this buffer is restaged one LP from now)
+      if constexpr (LATE) {
+        hn = unpack_header<L, T>(hB, lpB);
+        issue_tma_warp<L, T, P>(p, hn, buf, bar, policy, arr, lane);
+        ticket = atomic_add_if(p.counter, lane == 0, p.pk.zero);
+      }
     } else {
       // pair export: lanes 0/1 request perm[pos-4] now, store one LP later
       if (pend_lp >= 0 && lane < 2 && p.pair)
@@ -996,6 +1020,7 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
 #endif
     }
     h = hn;
+    if constexpr (DB) cur ^= 1;
   }
   if (pend_lp >= 0 && lane < 2 && p.pair) p.pair[2 * pend_lp + lane] = pair_code(pend_pos, pend_q);
 
