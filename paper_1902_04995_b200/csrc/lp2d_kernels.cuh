@@ -752,61 +752,38 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid
     const S* gy = static_cast<const S*>(p.ay) + h.off;
     const S* gb = static_cast<const S*>(p.b) + h.off;
     const P* gp = static_cast<const P*>(p.perm) + h.off;
-    const int mmax = __reduce_max_sync(kFull, (uint32_t)mj);
     uint32_t pmax = 0;
     decltype(float_bits(T(0))) sbits = float_bits(T(1));
-    // The permutation by 16-byte loads (segments start 8-element aligned and
-    // are padded to 8 elements: the layout contract), one batch of 8
-    // positions ahead of the data, which is gathered 8 positions (24
-    // independent loads) per round trip instead of one dependent perm -> data
-    // pair per position.
+    // The whole permutation by 16-byte loads (segments start 8-element
+    // aligned and are padded to 8 elements: the layout contract), then every
+    // constraint copied straight into the tile with cp.async (no registers,
+    // one round trip for the data), then the magnitude bound from the tile.
     constexpr int PV = 16 / (int)sizeof(P);  // permutation entries per vector
-    constexpr int GB = 8;                    // positions per gather batch
-    constexpr int VB = GB / PV;              // vectors per batch
-    uint4 wv[VB];
+    constexpr int NV = (MAXM + PV - 1) / PV;
+    uint4 wv[NV];
 #pragma unroll
-    for (int v = 0; v < VB; ++v)
+    for (int v = 0; v < NV; ++v)
       wv[v] = v * PV < mj ? __ldg(reinterpret_cast<const uint4*>(gp) + v) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-    for (int k0 = 0; k0 < MAXM; k0 += GB) {
-      if (k0 >= mmax) break;
-      uint32_t o[GB];
+    for (int v = 0; v < NV; ++v) {
+      const uint32_t ww[4] = {wv[v].x, wv[v].y, wv[v].z, wv[v].w};
 #pragma unroll
-      for (int v = 0; v < VB; ++v) {
-        const uint32_t ww[4] = {wv[v].x, wv[v].y, wv[v].z, wv[v].w};
-#pragma unroll
-        for (int e = 0; e < PV; ++e)
-          o[v * PV + e] = sizeof(P) == 2 ? ((ww[e / 2] >> (16 * (e & 1))) & 0xffffu) : ww[e];
-      }
-      // next batch's permutation vectors (off this batch's dependency chain)
-#pragma unroll
-      for (int v = 0; v < VB; ++v) {
-        const int e0 = k0 + GB + v * PV;
-        wv[v] = e0 < mj ? __ldg(reinterpret_cast<const uint4*>(gp + e0)) : make_uint4(0, 0, 0, 0);
-      }
-      T vx[GB], vy[GB], vb[GB];
-#pragma unroll
-      for (int u = 0; u < GB; ++u) {
-        const int k = k0 + u;
+      for (int e = 0; e < PV; ++e) {
+        const int k = v * PV + e;
         if (k < MAXM && k < mj) {
-          pmax = max(pmax, o[u]);
-          const uint32_t oc = min(o[u], (uint32_t)(mj - 1));
-          vx[u] = (T)gx[oc];
-          vy[u] = (T)gy[oc];
-          vb[u] = (T)gb[oc];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < GB; ++u) {
-        const int k = k0 + u;
-        if (k < MAXM && k < mj) {
-          sbits = max(sbits, float_bits(fabs(vx[u]) + fabs(vy[u])));
-          sx[at(4 + k, lane)] = (S)vx[u];
-          sy[at(4 + k, lane)] = (S)vy[u];
-          sb[at(4 + k, lane)] = (S)vb[u];
+          const uint32_t o = sizeof(P) == 2 ? ((ww[e / 2] >> (16 * (e & 1))) & 0xffffu) : ww[e];
+          pmax = max(pmax, o);
+          const uint32_t oc = min(o, (uint32_t)(mj - 1));
+          cp_async_elem(&sx[at(4 + k, lane)], gx + oc);
+          cp_async_elem(&sy[at(4 + k, lane)], gy + oc);
+          cp_async_elem(&sb[at(4 + k, lane)], gb + oc);
         }
       }
     }
+    cp_async_wait_all();
+#pragma unroll
+    for (int k = 0; k < MAXM; ++k)
+      if (k < mj) sbits = max(sbits, float_bits(fabs((T)sx[at(4 + k, lane)]) + fabs((T)sy[at(4 + k, lane)])));
     __syncwarp();
     const bool bad = live && (!h.ok || (mj > 0 && pmax >= (uint32_t)mj));
     const T m_all = float_from_bits<T>(sbits);
