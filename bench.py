@@ -369,7 +369,7 @@ def main():
                     help="scalar storage (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 5)")
-    ap.add_argument("--streams", type=int, default=2,
+    ap.add_argument("--streams", type=int, default=3,
                     help="streams the K timed steps alternate over (1 = back-to-back)")
     ap.add_argument("--full", action="store_true",
                     help="c3/c5: the config's full size (2^20 / 2^22 LPs) split over this "
