@@ -28,7 +28,7 @@ traffic["note"] = ("dram__bytes_read.sum + dram__bytes_write.sum of one launch o
                    "solve kernel, ncu --set full (profiles/r02_<tag>_ncu_summary.txt); keys: config, or "
                    "config-dtype for a non-default storage type")
 json.dump(traffic, open(os.path.join(PR, "traffic.json"), "w"), indent=1)
-out = ["| config | value (LP/s, device, 2-stream pipelined) | ms/step pipelined / isolated kernel | "
+out = ["| config | value (LP/s, device, 3-stream pipelined) | ms/step pipelined / isolated kernel | "
        "roofline frac (isolated kernel) | e2e LP/s (pinned host buffers, H2D+D2H in region) | e2e, "
        "permutations from seeds | reference arm LP/s (16 host threads) | e2e / reference |",
        "|---|---|---|---|---|---|---|---|"]
