@@ -927,7 +927,8 @@ bool host_pinned(const void* p) {
 
 // Per-device host-mode resources (grown on demand, kept across calls).
 struct HostPipe {
-  cudaStream_t copy = nullptr;
+  cudaStream_t copy = nullptr;  // host -> device
+  cudaStream_t back = nullptr;  // device -> host (the link is full duplex)
   cudaEvent_t h2d[2] = {}, solved[2] = {}, d2h[2] = {};
   void* pin_in[2] = {};
   size_t pin_in_bytes = 0;
@@ -974,6 +975,7 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   HostPipe& hp = g_pipe[dev];
   if (!hp.copy) {
     CUDA_TRY(cudaStreamCreateWithFlags(&hp.copy, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&hp.back, cudaStreamNonBlocking));
     for (int q = 0; q < 2; ++q) {
       CUDA_TRY(cudaEventCreateWithFlags(&hp.h2d[q], cudaEventDisableTiming));
       CUDA_TRY(cudaEventCreateWithFlags(&hp.solved[q], cudaEventDisableTiming));
@@ -1025,7 +1027,7 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   if (int rc = ensure_pinned(hp.pin_in, hp.pin_in_bytes, in_pinned ? al(o_in - o_m) : in_bytes)) return rc;
   if (!out_pinned)
     if (int rc = ensure_pinned(hp.pin_out, hp.pin_out_bytes, out_bytes + hist_bytes)) return rc;
-  cudaStream_t cs = d.stream, cp = hp.copy;
+  cudaStream_t cs = d.stream, cp = hp.copy, cb = hp.back;
   char* arena = static_cast<char*>(d.arena);
   std::vector<std::vector<uint32_t>> hist_host(2);
 
@@ -1037,6 +1039,7 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     char* D = arena + q * slot_bytes;
     char* H = static_cast<char*>(hp.pin_in[q]);
     CUDA_TRY(cudaEventSynchronize(hp.h2d[q]));  // the staging slot's previous DMA is done
+    CUDA_TRY(cudaStreamWaitEvent(cp, hp.solved[q], 0));  // chunk k-2 no longer reads device slot q
     const size_t sm_base = in_pinned ? o_m : 0;  // staged area starts at o_m when in_pinned
     int32_t* hm = reinterpret_cast<int32_t*>(H + (o_m - sm_base));
     int64_t* hoff = reinterpret_cast<int64_t*>(H + (o_off - sm_base));
@@ -1093,19 +1096,25 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     return 0;
   };
 
+  // Every wait is an event between the three streams except two host waits:
+  // staging reuse (upload k+2 waits for chunk k's H2D, which is queued behind
+  // nothing but other H2D) and the gather of chunk k-2 before chunk k's
+  // results land in the same host slot. Inputs stream back to back on the
+  // copy stream while the results go back on their own stream.
   if (nk > 0)
     if (int rc = upload(0)) return rc;
   for (int k = 0; k < nk; ++k) {
     const int q = k & 1;
-    if (k >= 1)
-      if (int rc = gather(k - 1)) return rc;  // frees staging slot (k+1) % 2
     if (k + 1 < nk)
-      if (int rc = upload(k + 1)) return rc;  // behind chunk k-1's results on the copy stream
+      if (int rc = upload(k + 1)) return rc;
+    if (k >= 2)
+      if (int rc = gather(k - 2)) return rc;  // frees host result slot q
     const int64_t c0 = cut[k], cnt = cut[k + 1] - c0;
     const int64_t E = b->offset[cut[k + 1]] - b->offset[c0];
     char* D = arena + q * slot_bytes;
     char* R = D + in_bytes;
     CUDA_TRY(cudaStreamWaitEvent(cs, hp.h2d[q], 0));
+    CUDA_TRY(cudaStreamWaitEvent(cs, hp.d2h[q], 0));  // chunk k-2's results are out of slot q
     if (b->perm_from_seed)
       if (int rc = shuffle_seeded(cnt, reinterpret_cast<const int32_t*>(D + o_m),
                                   reinterpret_cast<const int64_t*>(D + o_off), max_m, b->perm_seed,
@@ -1141,13 +1150,13 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     if (int rc = solve_device_batch<S>(kp, E, min_m, max_m, b->perm_bits, o->scheduler, dev, cs, true))
       return rc;
     CUDA_TRY(cudaEventRecord(hp.solved[q], cs));
-    CUDA_TRY(cudaStreamWaitEvent(cp, hp.solved[q], 0));
-    // results: D2H on the copy stream (behind chunk k+1's inputs)
+    CUDA_TRY(cudaStreamWaitEvent(cb, hp.solved[q], 0));
+    // results: D2H on the return stream
     char* dstp = static_cast<char*>(hp.pin_out[q]);
     auto d2h = [&](void* dst_user, size_t roff, size_t len) -> int {
       if (!len) return 0;
       void* dst = out_pinned ? dst_user : (void*)(dstp + roff);
-      CUDA_TRY(cudaMemcpyAsync(dst, R + roff, len, cudaMemcpyDeviceToHost, cp));
+      CUDA_TRY(cudaMemcpyAsync(dst, R + roff, len, cudaMemcpyDeviceToHost, cb));
       return 0;
     };
     int rc = d2h(out->status + c0, r_st, cnt);
@@ -1168,12 +1177,13 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
         hdst = dstp + out_bytes;
       }
       CUDA_TRY(cudaMemcpyAsync(hdst, kp.iter_hist, sizeof(uint32_t) * rows * hstride,
-                               cudaMemcpyDeviceToHost, cp));
+                               cudaMemcpyDeviceToHost, cb));
     }
-    CUDA_TRY(cudaEventRecord(hp.d2h[q], cp));
+    CUDA_TRY(cudaEventRecord(hp.d2h[q], cb));
   }
-  if (nk > 0)
-    if (int rc = gather(nk - 1)) return rc;
+  for (int k = std::max(0, nk - 2); k < nk; ++k)
+    if (int rc = gather(k)) return rc;
+  CUDA_TRY(cudaStreamSynchronize(cb));
   CUDA_TRY(cudaStreamSynchronize(cp));
   CUDA_TRY(cudaStreamSynchronize(cs));
   return 0;
