@@ -6,7 +6,9 @@
 // LP-index sharding over GPUs (one host thread per device) and, inside a GPU,
 // by warps claiming LPs from an atomic ticket.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -749,15 +751,18 @@ KParams make_params(const lp2d_opts* o) {
 
 // fp32 storage: widen the batch's scalars into double copies on the device
 // (k_widen), the input of the double kernels for those classes. kp's scalar
-// pointers are redirected to the copies carved from ws (5 arrays).
+// pointers are redirected to the copies carved from ws (5 arrays). The
+// element arrays cover offsets [e0, e0 + E) (a host-mode chunk addresses its
+// slot through pointers biased by -e0, so its offsets stay absolute).
 size_t widen_bytes(int64_t E, int64_t n) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   return 3 * al(sizeof(double) * E) + al(sizeof(double) * 2 * n) + al(sizeof(double) * n);
 }
 
-int widen_batch(KParams& kp, int64_t E, int64_t n, char* ws, int dev, cudaStream_t s) {
+int widen_batch(KParams& kp, int64_t E, int64_t e0, int64_t n, char* ws, int dev, cudaStream_t s) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const void* src[5] = {kp.ax, kp.ay, kp.b, kp.c, kp.bound_m};
+  const void* src[5] = {static_cast<const float*>(kp.ax) + e0, static_cast<const float*>(kp.ay) + e0,
+                        static_cast<const float*>(kp.b) + e0, kp.c, kp.bound_m};
   const int64_t cnt[5] = {E, E, E, 2 * n, n};
   void* dst[5];
   size_t o = 0;
@@ -773,9 +778,9 @@ int widen_batch(KParams& kp, int64_t E, int64_t n, char* ws, int dev, cudaStream
     note_launch();
   }
   CUDA_TRY(cudaGetLastError());
-  kp.ax = dst[0];
-  kp.ay = dst[1];
-  kp.b = dst[2];
+  kp.ax = static_cast<double*>(dst[0]) - e0;
+  kp.ay = static_cast<double*>(dst[1]) - e0;
+  kp.b = static_cast<double*>(dst[2]) - e0;
   kp.c = dst[3];
   kp.bound_m = dst[4];
   return 0;
@@ -783,7 +788,7 @@ int widen_batch(KParams& kp, int64_t E, int64_t n, char* ws, int dev, cudaStream
 
 // Solve of a device-resident batch with scalars stored as S (float or
 // double); the arithmetic is the reference's double in both cases and the
-// outputs are double. E = scalar elements (offset[n]).
+// outputs are double. E = scalar elements (offset[n] - offset[0]), e0 = offset[0].
 template <typename P>
 int solve_f32_balanced(KParams kp, int64_t E, int64_t min_m, int64_t max_m, int dev,
                        cudaStream_t s, bool may_sync) {
@@ -806,8 +811,8 @@ int solve_f32_balanced(KParams kp, int64_t E, int64_t min_m, int64_t max_m, int 
 }
 
 template <typename S>
-int solve_device_batch(KParams kp, int64_t E, int64_t min_m, int64_t max_m, int perm_bits,
-                       int sched, int dev, cudaStream_t s, bool may_sync) {
+int solve_device_batch(KParams kp, int64_t E, int64_t e0, int64_t min_m, int64_t max_m,
+                       int perm_bits, int sched, int dev, cudaStream_t s, bool may_sync) {
   if constexpr (sizeof(S) == 4) {
     if (sched == LP2D_SCHED_BALANCED) {
       if (perm_bits == 16) return solve_f32_balanced<uint16_t>(kp, E, min_m, max_m, dev, s, may_sync);
@@ -815,7 +820,7 @@ int solve_device_batch(KParams kp, int64_t E, int64_t min_m, int64_t max_m, int 
     }
     void* ws = nullptr;
     CUDA_TRY(cudaMallocFromPoolAsync(&ws, widen_bytes(E, kp.n_list), g_dev[dev].pool, s));
-    int rc = widen_batch(kp, E, kp.n_list, static_cast<char*>(ws), dev, s);
+    int rc = widen_batch(kp, E, e0, kp.n_list, static_cast<char*>(ws), dev, s);
     if (rc == 0) rc = launch_solve<double>(kp, min_m, max_m, perm_bits, sched, dev, s, may_sync);
     CUDA_TRY(cudaFreeAsync(ws, s));
     return rc;
@@ -926,6 +931,44 @@ bool host_pinned(const void* p) {
 }
 
 // Per-device host-mode resources (grown on demand, kept across calls).
+// LP2D_B200_TRACE=1: per-chunk timeline of the host pipeline on stderr
+// (device events on the three streams, relative to the call's first H2D).
+struct PipeTrace {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<std::string> what;
+  void mark(cudaStream_t s, const std::string& w) {
+    if (!on) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    ev.push_back(e);
+    what.push_back(w);
+  }
+  void dump() {
+    if (!on || ev.empty()) return;
+    cudaEventSynchronize(ev.back());
+    for (size_t i = 0; i < ev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[0], ev[i]);
+      std::fprintf(stderr, "[lp2d trace] %8.3f ms  %s\n", ms, what[i].c_str());
+    }
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    ev.clear();
+  }
+};
+bool trace_on() {
+  static const bool on = std::getenv("LP2D_B200_TRACE") && std::getenv("LP2D_B200_TRACE")[0] == '1';
+  return on;
+}
+double host_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+void trace_host(const char* what, double t0) {
+  if (trace_on()) std::fprintf(stderr, "[lp2d trace] host %8.3f ms  %s\n", host_ms() - t0, what);
+}
+
 struct HostPipe {
   cudaStream_t copy = nullptr;  // host -> device
   cudaStream_t back = nullptr;  // device -> host (the link is full duplex)
@@ -949,6 +992,35 @@ int ensure_pinned(void** slot, size_t& have, size_t want) {
   return 0;
 }
 
+// The host-mode layout contract over LPs [lo, hi) (one branch-free pass; the
+// slow scan only runs to name the first offending LP), with the range's
+// smallest and largest m.
+int scan_layout(const lp2d_batch_soa* b, int64_t lo, int64_t hi, int64_t& min_m, int64_t& max_m) {
+  int32_t mx = 0, mn = INT32_MAX;
+  uint64_t bad = 0;
+  for (int64_t j = lo; j < hi; ++j) {
+    const int32_t mj = b->m[j];
+    const int64_t o0 = b->offset[j], o1 = b->offset[j + 1];
+    bad |= (uint64_t)(mj < 0) | (uint64_t)(o0 & 7) | (uint64_t)(o1 - o0 < (((int64_t)mj + 7) & ~int64_t(7)));
+    mx = std::max(mx, mj);
+    mn = std::min(mn, mj);
+  }
+  if (bad) {
+    for (int64_t j = lo; j < hi; ++j) {
+      const int64_t mj = b->m[j];
+      if (mj < 0) return fail(LP2D_ERR_PERM_LENGTH, "negative constraint count");
+      const int64_t cap8 = (mj + 7) & ~int64_t(7);
+      if ((b->offset[j] & 7) != 0 || b->offset[j + 1] - b->offset[j] < cap8)
+        return fail(LP2D_ERR_LAYOUT, "offset[" + std::to_string(j) +
+                                         "] violates the 8-element layout contract");
+    }
+  }
+  if (b->perm_bits == 16 && mx > 65536) return fail(LP2D_ERR_ARG, "u16 permutations need m <= 65536");
+  min_m = mn;
+  max_m = mx;
+  return 0;
+}
+
 template <typename S>
 int solve_shard_mock(int dev, const lp2d_batch_soa* b, lp2d_out* out, int64_t lo, int64_t hi) {
   const std::vector<int64_t> cut = plan_chunks(b->offset, lo, hi, chunk_elems());
@@ -967,7 +1039,14 @@ template <typename S>
 int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out,
                      int64_t lo, int64_t hi, int64_t min_m, int64_t max_m) {
   using T = double;  // outputs
-  if (mock_devices()) return solve_shard_mock<S>(dev, b, out, lo, hi);
+  const double th0 = host_ms();
+  // min_m < 0: the caller left the layout check to the pipeline (per chunk)
+  const bool lazy = min_m < 0;
+  if (mock_devices()) {
+    if (lazy)
+      if (int rc = scan_layout(b, lo, hi, min_m, max_m)) return rc;
+    return solve_shard_mock<S>(dev, b, out, lo, hi);
+  }
   if (int rc = ensure_device(dev)) return rc;
   DeviceState& d = g_dev[dev];
   std::lock_guard<std::mutex> lock(d.mu);
@@ -1023,8 +1102,13 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   const bool out_pinned = host_pinned(out->status) && host_pinned(out->x) && host_pinned(out->y) &&
                           host_pinned(out->value) && host_pinned(out->pair) &&
                           host_pinned(out->violation_events) && host_pinned(out->work_units);
-  // the small per-chunk arrays (m, rebased offsets) always go through staging
-  if (int rc = ensure_pinned(hp.pin_in, hp.pin_in_bytes, in_pinned ? al(o_in - o_m) : in_bytes)) return rc;
+  // m and the offsets go to the device as they are (the chunk's element
+  // arrays are addressed through pointers biased by -offset[c0]); staged only
+  // when the caller's copies are pageable
+  const bool mo_pinned = host_pinned(b->m) && host_pinned(b->offset);
+  const size_t stage_bytes = in_pinned ? (mo_pinned ? 0 : al(o_in - o_m)) : in_bytes;
+  if (stage_bytes)
+    if (int rc = ensure_pinned(hp.pin_in, hp.pin_in_bytes, stage_bytes)) return rc;
   if (!out_pinned)
     if (int rc = ensure_pinned(hp.pin_out, hp.pin_out_bytes, out_bytes + hist_bytes)) return rc;
   cudaStream_t cs = d.stream, cp = hp.copy, cb = hp.back;
@@ -1032,38 +1116,43 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   std::vector<std::vector<uint32_t>> hist_host(2);
 
   // stage + enqueue the H2D of chunk k into slot k % 2
+  std::vector<int64_t> kmin(nk, min_m), kmax(nk, max_m);
   auto upload = [&](int k) -> int {
     const int q = k & 1;
     const int64_t c0 = cut[k], c1 = cut[k + 1], cnt = c1 - c0;
+    if (lazy)
+      if (int rc = scan_layout(b, c0, c1, kmin[k], kmax[k])) {
+        // (earlier chunks are in flight: drain them before reporting)
+        cudaStreamSynchronize(cp);
+        cudaStreamSynchronize(cs);
+        cudaStreamSynchronize(cb);
+        return rc;
+      }
     const int64_t e0 = b->offset[c0], E = b->offset[c1] - e0;
     char* D = arena + q * slot_bytes;
     char* H = static_cast<char*>(hp.pin_in[q]);
     CUDA_TRY(cudaEventSynchronize(hp.h2d[q]));  // the staging slot's previous DMA is done
     CUDA_TRY(cudaStreamWaitEvent(cp, hp.solved[q], 0));  // chunk k-2 no longer reads device slot q
     const size_t sm_base = in_pinned ? o_m : 0;  // staged area starts at o_m when in_pinned
-    int32_t* hm = reinterpret_cast<int32_t*>(H + (o_m - sm_base));
-    int64_t* hoff = reinterpret_cast<int64_t*>(H + (o_off - sm_base));
-    std::memcpy(hm, b->m + c0, sizeof(int32_t) * cnt);
-    for (int64_t j = 0; j <= cnt; ++j) hoff[j] = b->offset[c0 + j] - e0;
-    const void* src[6] = {static_cast<const S*>(b->ax) + e0, static_cast<const S*>(b->ay) + e0,
+    const void* src[8] = {static_cast<const S*>(b->ax) + e0, static_cast<const S*>(b->ay) + e0,
                           static_cast<const S*>(b->b) + e0,
                           b->perm ? static_cast<const char*>(b->perm) + ps * e0 : nullptr,
                           static_cast<const S*>(b->c) + 2 * c0,
-                          static_cast<const S*>(b->bound_m) + c0};
-    const size_t dst[6] = {o_ax, o_ay, o_b, o_perm, o_c, o_M};
-    const size_t len[6] = {sizeof(S) * E, sizeof(S) * E, sizeof(S) * E, ps * E,
-                           sizeof(S) * 2 * cnt, sizeof(S) * cnt};
-    for (int a = 0; a < 6; ++a) {
+                          static_cast<const S*>(b->bound_m) + c0, b->m + c0, b->offset + c0};
+    const size_t dst[8] = {o_ax, o_ay, o_b, o_perm, o_c, o_M, o_m, o_off};
+    const size_t len[8] = {sizeof(S) * E, sizeof(S) * E, sizeof(S) * E, ps * E,
+                           sizeof(S) * 2 * cnt, sizeof(S) * cnt, sizeof(int32_t) * cnt,
+                           sizeof(int64_t) * (cnt + 1)};
+    for (int a = 0; a < 8; ++a) {
       if (!len[a] || (a == 3 && b->perm_from_seed)) continue;  // (perms generated on the device)
-      if (in_pinned) {
+      if (a < 6 ? in_pinned : mo_pinned) {
         CUDA_TRY(cudaMemcpyAsync(D + dst[a], src[a], len[a], cudaMemcpyHostToDevice, cp));
       } else {
-        std::memcpy(H + dst[a], src[a], len[a]);
-        CUDA_TRY(cudaMemcpyAsync(D + dst[a], H + dst[a], len[a], cudaMemcpyHostToDevice, cp));
+        char* h = H + (dst[a] - sm_base);
+        std::memcpy(h, src[a], len[a]);
+        CUDA_TRY(cudaMemcpyAsync(D + dst[a], h, len[a], cudaMemcpyHostToDevice, cp));
       }
     }
-    CUDA_TRY(cudaMemcpyAsync(D + o_m, hm, (o_off - o_m) + sizeof(int64_t) * (cnt + 1),
-                             cudaMemcpyHostToDevice, cp));
     CUDA_TRY(cudaEventRecord(hp.h2d[q], cp));
     return 0;
   };
@@ -1101,24 +1190,37 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   // nothing but other H2D) and the gather of chunk k-2 before chunk k's
   // results land in the same host slot. Inputs stream back to back on the
   // copy stream while the results go back on their own stream.
+  trace_host("shard setup", th0);
+  PipeTrace tr;
+  tr.on = trace_on();
+  tr.mark(cp, "start");
   if (nk > 0)
     if (int rc = upload(0)) return rc;
+  tr.mark(cp, "h2d 0 done");
   for (int k = 0; k < nk; ++k) {
     const int q = k & 1;
-    if (k + 1 < nk)
+    if (k + 1 < nk) {
       if (int rc = upload(k + 1)) return rc;
+      tr.mark(cp, "h2d " + std::to_string(k + 1) + " done");
+    }
     if (k >= 2)
       if (int rc = gather(k - 2)) return rc;  // frees host result slot q
     const int64_t c0 = cut[k], cnt = cut[k + 1] - c0;
-    const int64_t E = b->offset[cut[k + 1]] - b->offset[c0];
+    const int64_t e0 = b->offset[c0], E = b->offset[cut[k + 1]] - e0;
     char* D = arena + q * slot_bytes;
     char* R = D + in_bytes;
+    // element arrays addressed by the chunk's absolute offsets
+    char* const dax = D + o_ax - (int64_t)sizeof(S) * e0;
+    char* const day = D + o_ay - (int64_t)sizeof(S) * e0;
+    char* const db = D + o_b - (int64_t)sizeof(S) * e0;
+    char* const dperm = D + o_perm - (int64_t)ps * e0;
     CUDA_TRY(cudaStreamWaitEvent(cs, hp.h2d[q], 0));
     CUDA_TRY(cudaStreamWaitEvent(cs, hp.d2h[q], 0));  // chunk k-2's results are out of slot q
+    tr.mark(cs, "solve " + std::to_string(k) + " start");
     if (b->perm_from_seed)
       if (int rc = shuffle_seeded(cnt, reinterpret_cast<const int32_t*>(D + o_m),
-                                  reinterpret_cast<const int64_t*>(D + o_off), max_m, b->perm_seed,
-                                  b->perm_first + c0, b->perm_mul, b->perm_add, D + o_perm,
+                                  reinterpret_cast<const int64_t*>(D + o_off), kmax[k], b->perm_seed,
+                                  b->perm_first + c0, b->perm_mul, b->perm_add, dperm,
                                   b->perm_bits, cs))
         return rc;
     KParams kp = make_params<T>(o);
@@ -1126,10 +1228,10 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     kp.list = nullptr;
     kp.m = reinterpret_cast<const int32_t*>(D + o_m);
     kp.offset = reinterpret_cast<const int64_t*>(D + o_off);
-    kp.ax = D + o_ax;
-    kp.ay = D + o_ay;
-    kp.b = D + o_b;
-    kp.perm = D + o_perm;
+    kp.ax = dax;
+    kp.ay = day;
+    kp.b = db;
+    kp.perm = dperm;
     kp.c = D + o_c;
     kp.bound_m = D + o_M;
     kp.status = reinterpret_cast<uint8_t*>(R + r_st);
@@ -1147,9 +1249,11 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
       kp.hist_stride = (int32_t)hstride;
       CUDA_TRY(cudaMemsetAsync(kp.iter_hist, 0, sizeof(uint32_t) * rows * hstride, cs));
     }
-    if (int rc = solve_device_batch<S>(kp, E, min_m, max_m, b->perm_bits, o->scheduler, dev, cs, true))
+    if (int rc = solve_device_batch<S>(kp, E, e0, kmin[k], kmax[k], b->perm_bits, o->scheduler, dev,
+                                       cs, true))
       return rc;
     CUDA_TRY(cudaEventRecord(hp.solved[q], cs));
+    tr.mark(cs, "solve " + std::to_string(k) + " done");
     CUDA_TRY(cudaStreamWaitEvent(cb, hp.solved[q], 0));
     // results: D2H on the return stream
     char* dstp = static_cast<char*>(hp.pin_out[q]);
@@ -1180,12 +1284,16 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
                                cudaMemcpyDeviceToHost, cb));
     }
     CUDA_TRY(cudaEventRecord(hp.d2h[q], cb));
+    tr.mark(cb, "d2h " + std::to_string(k) + " done");
   }
   for (int k = std::max(0, nk - 2); k < nk; ++k)
     if (int rc = gather(k)) return rc;
   CUDA_TRY(cudaStreamSynchronize(cb));
   CUDA_TRY(cudaStreamSynchronize(cp));
+  trace_host("pipeline enqueued", th0);
   CUDA_TRY(cudaStreamSynchronize(cs));
+  trace_host("pipeline done", th0);
+  tr.dump();
   return 0;
 }
 
@@ -1244,31 +1352,25 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
     if constexpr (sizeof(S) == 4) {
       CUDA_TRY(cudaMemcpy(&E, b->offset + b->n, sizeof(int64_t), cudaMemcpyDeviceToHost));
     }
-    return solve_device_batch<S>(kp, E, b->min_m, b->max_m, b->perm_bits, o->scheduler, dev,
+    return solve_device_batch<S>(kp, E, 0, b->min_m, b->max_m, b->perm_bits, o->scheduler, dev,
                                  static_cast<cudaStream_t>(o->stream), false);
   }
-  // host mode: validate the layout contract, then shard.
-  int64_t max_m = 0, min_m = INT64_MAX;
-  for (int64_t j = 0; j < b->n; ++j) {
-    const int64_t mj = b->m[j];
-    if (mj < 0) return fail(LP2D_ERR_PERM_LENGTH, "negative constraint count");
-    const int64_t cap8 = (mj + 7) & ~int64_t(7);
-    if ((b->offset[j] & 7) != 0 || b->offset[j + 1] - b->offset[j] < cap8)
-      return fail(LP2D_ERR_LAYOUT, "offset[" + std::to_string(j) +
-                                       "] violates the 8-element layout contract");
-    max_m = std::max(max_m, mj);
-    min_m = std::min(min_m, mj);
-  }
-  if (b->perm_bits == 16 && max_m > 65536)
-    return fail(LP2D_ERR_ARG, "u16 permutations need m <= 65536");
+  const double th0 = host_ms();
+  // host mode: validate the layout contract, then shard. A single-GPU solve
+  // without lane histograms validates chunk by chunk inside the pipeline
+  // (overlapped with the previous chunk's transfer); otherwise up front.
+  int use = o->n_gpus > 0 ? std::min(o->n_gpus, ndev) : ndev;
+  use = (int)std::min<int64_t>(std::min(use, 64), b->n);
+  if (use == 1 && !out->iter_hist) return solve_shard_host<S>(0, b, o, out, 0, b->n, -1, -1);
+  int64_t min_m = 0, max_m = 0;
+  if (int rc = scan_layout(b, 0, b->n, min_m, max_m)) return rc;
+  trace_host("validated", th0);
   if (out->iter_hist)
     std::memset(out->iter_hist, 0,
                 sizeof(uint32_t) * ((b->n + o->block_width - 1) / o->block_width) * (max_m + 1));
-  int use = o->n_gpus > 0 ? std::min(o->n_gpus, ndev) : ndev;
-  use = (int)std::min<int64_t>(std::min(use, 64), b->n);
+  if (use == 1) return solve_shard_host<S>(0, b, o, out, 0, b->n, min_m, max_m);
   std::vector<int64_t> cut(use + 1, 0);
   lp2dgpu_partition(b->n, b->m, use, cut.data());
-  if (use == 1) return solve_shard_host<S>(0, b, o, out, 0, b->n, min_m, max_m);
   std::vector<int> rcs(use, 0);
   std::vector<std::string> errs(use);
   std::vector<std::thread> th;
@@ -1306,14 +1408,19 @@ int lp2dgpu_solve_f64(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out
 
 int lp2dgpu_partition(int64_t n, const int32_t* m, int32_t parts, int64_t* cut) {
   if (n < 0 || parts < 1 || !cut || (n > 0 && !m)) return fail(LP2D_ERR_ARG, "bad partition arguments");
-  double total = 0;
-  for (int64_t j = 0; j < n; ++j) total += (double)std::max(m[j], 0) + 4.0;
+  // cut k: the first prefix whose weight sum(m + 4) reaches total * k / parts
+  // (integer sums; the thresholds are the double quotients rounded up)
+  int64_t tot = 0;
+  for (int64_t j = 0; j < n; ++j) tot += (int64_t)std::max(m[j], 0) + 4;
+  const double total = (double)tot;
+  std::vector<int64_t> thr(parts + 1);
+  for (int k = 1; k < parts; ++k) thr[k] = (int64_t)std::ceil(total * k / parts);
   cut[0] = 0;
   int k = 1;
-  double acc = 0;
+  int64_t acc = 0;
   for (int64_t j = 0; j < n && k < parts; ++j) {
-    acc += (double)std::max(m[j], 0) + 4.0;
-    while (k < parts && acc >= total * k / parts) cut[k++] = j + 1;
+    acc += (int64_t)std::max(m[j], 0) + 4;
+    while (k < parts && acc >= thr[k]) cut[k++] = j + 1;
   }
   for (; k <= parts; ++k) cut[k] = n;
   return 0;
