@@ -151,8 +151,12 @@ void lp2dgpu_default_opts(lp2d_opts* opts);
  * chunks (LP2D_B200_CHUNK_ELEMS elements, default 4 Mi) pipelined over two
  * device slots (H2D of the next chunk overlaps the solve of the current one;
  * pageable inputs are staged through pinned buffers, pinned ones are DMA'd
- * directly); returns when every result is in place. Device mode: enqueues on
- * opts->stream and returns without synchronising. */
+ * directly; results return on a second copy stream); returns when every
+ * result is in place. The layout contract is checked before any LP of a
+ * chunk is sent (single-GPU calls check chunk by chunk, so on an error the
+ * outputs of earlier chunks may already be written: outputs are unspecified
+ * after any error). Device mode: enqueues on opts->stream and returns
+ * without synchronising. */
 int lp2dgpu_solve_f32(const lp2d_batch_soa* batch, const lp2d_opts* opts,
                       lp2d_out* out);
 int lp2dgpu_solve_f64(const lp2d_batch_soa* batch, const lp2d_opts* opts,
