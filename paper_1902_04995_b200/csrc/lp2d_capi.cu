@@ -1102,6 +1102,11 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   const bool out_pinned = host_pinned(out->status) && host_pinned(out->x) && host_pinned(out->y) &&
                           host_pinned(out->value) && host_pinned(out->pair) &&
                           host_pinned(out->violation_events) && host_pinned(out->work_units);
+  // Results come back through the pinned staging slot (ONE copy of the
+  // chunk's result block, then host copies) when the caller's arrays are
+  // pageable or the block is small (per-copy latency beats bandwidth there);
+  // otherwise straight into the caller's pinned arrays.
+  const bool direct_out = out_pinned && out_bytes + hist_bytes > (size_t(1) << 20);
   // m and the offsets go to the device as they are (the chunk's element
   // arrays are addressed through pointers biased by -offset[c0]); staged only
   // when the caller's copies are pageable
@@ -1109,7 +1114,7 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
   const size_t stage_bytes = in_pinned ? (mo_pinned ? 0 : al(o_in - o_m)) : in_bytes;
   if (stage_bytes)
     if (int rc = ensure_pinned(hp.pin_in, hp.pin_in_bytes, stage_bytes)) return rc;
-  if (!out_pinned)
+  if (!direct_out)
     if (int rc = ensure_pinned(hp.pin_out, hp.pin_out_bytes, out_bytes + hist_bytes)) return rc;
   cudaStream_t cs = d.stream, cp = hp.copy, cb = hp.back;
   char* arena = static_cast<char*>(d.arena);
@@ -1162,7 +1167,7 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     const int64_t c0 = cut[k], cnt = cut[k + 1] - c0;
     CUDA_TRY(cudaEventSynchronize(hp.d2h[q]));
     const int64_t row0 = c0 / W, rows = out->iter_hist ? (cut[k + 1] - 1) / W - row0 + 1 : 0;
-    if (!out_pinned) {
+    if (!direct_out) {
       const char* R = static_cast<const char*>(hp.pin_out[q]);
       std::memcpy(out->status + c0, R + r_st, cnt);
       std::memcpy(static_cast<T*>(out->x) + c0, R + r_x, sizeof(T) * cnt);
@@ -1175,7 +1180,7 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     }
     if (rows) {
       // chunks and shards may share a block row: accumulate (zeroed by the caller)
-      const uint32_t* hsrc = out_pinned ? hist_host[q].data()
+      const uint32_t* hsrc = direct_out ? hist_host[q].data()
                                         : reinterpret_cast<const uint32_t*>(
                                               static_cast<const char*>(hp.pin_out[q]) + out_bytes);
       static std::mutex hist_mu;
@@ -1258,11 +1263,11 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     // results: D2H on the return stream
     char* dstp = static_cast<char*>(hp.pin_out[q]);
     auto d2h = [&](void* dst_user, size_t roff, size_t len) -> int {
-      if (!len) return 0;
-      void* dst = out_pinned ? dst_user : (void*)(dstp + roff);
-      CUDA_TRY(cudaMemcpyAsync(dst, R + roff, len, cudaMemcpyDeviceToHost, cb));
+      if (!len || !direct_out) return 0;
+      CUDA_TRY(cudaMemcpyAsync(dst_user, R + roff, len, cudaMemcpyDeviceToHost, cb));
       return 0;
     };
+    if (!direct_out) CUDA_TRY(cudaMemcpyAsync(dstp, R, out_bytes, cudaMemcpyDeviceToHost, cb));
     int rc = d2h(out->status + c0, r_st, cnt);
     if (!rc) rc = d2h(static_cast<T*>(out->x) + c0, r_x, sizeof(T) * cnt);
     if (!rc) rc = d2h(static_cast<T*>(out->y) + c0, r_y, sizeof(T) * cnt);
@@ -1274,7 +1279,7 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     if (rc) return rc;
     if (rows) {
       void* hdst;
-      if (out_pinned) {
+      if (direct_out) {
         hist_host[q].assign((size_t)(rows * hstride), 0u);
         hdst = hist_host[q].data();  // (pageable: this copy completes before returning)
       } else {
