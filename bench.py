@@ -245,6 +245,8 @@ def make_batch(cfg_name, rank, dt, via="ours", n=None, first=None):
     (tests/test_generate.py)."""
     n_cfg = CONFIGS[cfg_name][0]
     if first is None:
+        if n is None and n_cfg == 0:  # heavy-tailed: every rank draws the same size list
+            n = len(config_layout(cfg_name, 0, None, via)[0])
         first = rank * (n if n is not None else n_cfg)
     sizes, kind, bscale, seed = config_layout(cfg_name, first, n, via)
     if via == "reference":

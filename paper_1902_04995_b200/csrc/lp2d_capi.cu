@@ -67,6 +67,13 @@ struct DeviceState {
   std::mutex fork_mu;
   cudaStream_t cls_stream[16] = {};
   cudaEvent_t cls_event[17] = {};
+  // Host mode with perm_from_seed: the large LPs' permutations are shuffled
+  // on aux while the rest of the chunk proceeds; only size classes that can
+  // hold an LP with m > perm_wait_m wait for perm_ev (set by shuffle_seeded,
+  // consumed by launch_binned; under mu, the host thread owns the device).
+  cudaStream_t aux = nullptr;
+  cudaEvent_t perm_ev = nullptr;
+  int64_t perm_wait_m = INT64_MAX;
   // Stream-ordered workspace pool (binning lists) that keeps its memory:
   // the default pool returns freed memory at every synchronisation, making
   // the next allocation remap it (milliseconds, randomly).
@@ -98,6 +105,8 @@ int ensure_device(int dev) {
   CUDA_TRY(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
   for (auto& cs : d.cls_stream) CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   for (auto& ce : d.cls_event) CUDA_TRY(cudaEventCreateWithFlags(&ce, cudaEventDisableTiming));
+  CUDA_TRY(cudaStreamCreateWithFlags(&d.aux, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&d.perm_ev, cudaEventDisableTiming));
   cudaMemPoolProps props = {};
   props.allocType = cudaMemAllocationTypePinned;
   props.location.type = cudaMemLocationTypeDevice;
@@ -568,7 +577,14 @@ int launch_binned(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStream_
                   bool may_sync, F&& launch_cls) {
   const int cmin = class_of<T>(std::max<int64_t>(min_m, 0));
   const int cmax = class_of<T>(max_m);
-  if (cmin == cmax) return launch_cls(kp, cmax, dev, s, max_m);
+  DeviceState& dv = g_dev[dev];
+  const int64_t perm_wait_m = dv.perm_wait_m;
+  dv.perm_wait_m = INT64_MAX;
+  const bool perm_wait = perm_wait_m != INT64_MAX;
+  if (cmin == cmax) {
+    if (perm_wait) CUDA_TRY(cudaStreamWaitEvent(s, dv.perm_ev, 0));
+    return launch_cls(kp, cmax, dev, s, max_m);
+  }
   // Mixed sizes: bin LP ids by class on the device, one launch per class.
   BinSpec spec{};
   spec.nreg = n_reg_classes<T>();
@@ -643,6 +659,9 @@ int launch_binned(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStream_
       if (may_sync) kc.n_list = n_host;
       cudaStream_t cs = d.cls_stream[sidx];
       CUDA_TRY(cudaStreamWaitEvent(cs, d.cls_event[16], 0));
+      // (LPs above perm_wait_m get their permutations from the aux stream)
+      if (perm_wait && (c >= spec.nreg || 32 * kSlotClasses[c] - 4 > perm_wait_m))
+        CUDA_TRY(cudaStreamWaitEvent(cs, d.perm_ev, 0));
       int r = launch_cls(kc, c, dev, cs, cap_m);
       CUDA_TRY(cudaEventRecord(d.cls_event[sidx], cs));
       CUDA_TRY(cudaStreamWaitEvent(s, d.cls_event[sidx], 0));
@@ -664,6 +683,7 @@ int launch_binned(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStream_
       rc = launch_one(c, lo, hi, host_counts[c], max_m, c);
     }
   }
+  if (perm_wait) CUDA_TRY(cudaStreamWaitEvent(s, dv.perm_ev, 0));
   CUDA_TRY(cudaFreeAsync(ws, s));
   return rc;
 }
@@ -831,13 +851,15 @@ int solve_device_batch(KParams kp, int64_t E, int64_t e0, int64_t min_m, int64_t
 
 // Permutations of LPs [0, n) of a (sub)batch from seeds, global index
 // first + j (k_shuffle_seeded), into perm (device), on stream s.
-int shuffle_seeded(int64_t n, const int32_t* m, const int64_t* offset, int64_t max_m,
+int shuffle_seeded(bool split, int64_t n, const int32_t* m, const int64_t* offset, int64_t max_m,
                    uint64_t seed, int64_t first, int32_t mul, int32_t add, void* perm,
                    int32_t perm_bits, cudaStream_t s) {
   if (n <= 0) return 0;
   const size_t es = perm_bits / 8;
-  // shared-memory slices of up to 1024 entries (LPs above shuffle in global
-  // memory), so a few large LPs do not push a mixed batch out of smem
+  // shared-memory slices of up to 1024 entries per thread, so a few large
+  // LPs do not push a mixed batch out of smem; LPs above get a CTA each
+  // (k_shuffle_seeded_big, the whole permutation in smem), and LPs beyond
+  // 200 KB of entries shuffle in place in global memory
   int32_t ps = (int32_t)(((std::min<int64_t>(std::max<int64_t>(max_m, 1), 1024) + 7) / 8) * 8);
   int threads = (int)std::min<int64_t>(128, (int64_t)(200 * 1024 / (ps * es)) & ~int64_t(31));
   if (threads < 32) {  // large LPs: in place in global memory
@@ -847,26 +869,56 @@ int shuffle_seeded(int64_t n, const int32_t* m, const int64_t* offset, int64_t m
   const size_t smem = (size_t)threads * ps * es;
   const unsigned grid = (unsigned)((n + threads - 1) / threads);
   // (the dynamic shared-memory opt-in, once per device and kernel: 200 KB)
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
   {
     static bool done[64] = {};
     static std::mutex mu;
-    int dev = 0;
-    CUDA_TRY(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lock(mu);
     if (dev >= 0 && dev < 64 && !done[dev]) {
       CUDA_TRY(cudaFuncSetAttribute(k_shuffle_seeded<uint16_t>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       CUDA_TRY(cudaFuncSetAttribute(k_shuffle_seeded<uint32_t>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      CUDA_TRY(cudaFuncSetAttribute(k_shuffle_seeded_big<uint16_t>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      CUDA_TRY(cudaFuncSetAttribute(k_shuffle_seeded_big<uint32_t>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       done[dev] = true;
     }
   }
+  const int32_t big_lo = ps;
+  const int32_t big_hi =
+      (int32_t)std::min<int64_t>(max_m, (int64_t)(200 * 1024 / es) & ~int64_t(7));
+  if (ps > 0 && big_hi > big_lo) {
+    const size_t bsm = ((size_t)big_hi * es + 15) & ~size_t(15);
+    const unsigned bgrid = (unsigned)std::min<int64_t>(n, 64 * (int64_t)std::max(1, g_dev[dev].sm_count));
+    DeviceState& dv = g_dev[dev];
+    cudaStream_t bs = s;
+    if (split) {  // fork onto aux; launch_binned makes the large classes wait
+      CUDA_TRY(cudaEventRecord(dv.perm_ev, s));
+      CUDA_TRY(cudaStreamWaitEvent(dv.aux, dv.perm_ev, 0));
+      bs = dv.aux;
+    }
+    if (perm_bits == 16)
+      k_shuffle_seeded_big<uint16_t><<<bgrid, 64, bsm, bs>>>(n, m, offset, seed, first, mul, add,
+                                                              static_cast<uint16_t*>(perm), big_lo, big_hi);
+    else
+      k_shuffle_seeded_big<uint32_t><<<bgrid, 64, bsm, bs>>>(n, m, offset, seed, first, mul, add,
+                                                              static_cast<uint32_t*>(perm), big_lo, big_hi);
+    note_launch();
+    if (split) {
+      CUDA_TRY(cudaEventRecord(dv.perm_ev, dv.aux));
+      dv.perm_wait_m = big_lo;
+    }
+  }
+  const int32_t skip_hi = (ps > 0 && big_hi > big_lo) ? big_hi : big_lo;
   if (perm_bits == 16)
     k_shuffle_seeded<uint16_t><<<grid, threads, smem, s>>>(n, m, offset, seed, first, mul, add,
-                                                           static_cast<uint16_t*>(perm), ps);
+                                                           static_cast<uint16_t*>(perm), ps, big_lo, skip_hi);
   else
     k_shuffle_seeded<uint32_t><<<grid, threads, smem, s>>>(n, m, offset, seed, first, mul, add,
-                                                           static_cast<uint32_t*>(perm), ps);
+                                                           static_cast<uint32_t*>(perm), ps, big_lo, skip_hi);
   note_launch();
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -876,11 +928,12 @@ int shuffle_seeded(int64_t n, const int32_t* m, const int64_t* offset, int64_t m
 // The shard is cut into chunks of at most chunk_elems() constraint elements
 // and pipelined over two device slots: H2D of chunk k+1 (copy stream) runs
 // while chunk k is solved (compute stream), and chunk k's results come back
-// on the copy stream behind chunk k+1's inputs. Inputs in pageable memory are
+// on a third stream (the link is full duplex). Inputs in pageable memory are
 // staged through two pinned buffers (filled by this shard's host thread while
 // the previous chunk's DMA runs); pinned (page-locked / registered) inputs are
-// DMA'd directly. Results go to pinned staging and are copied out after their
-// D2H completes, or straight into pinned result buffers.
+// DMA'd directly. Results go to pinned staging (one copy per chunk) and are
+// copied out after their D2H completes, or, for large pinned result arrays,
+// straight into them.
 
 int64_t chunk_elems() {
   static const int64_t v = [] {
@@ -1223,7 +1276,7 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     CUDA_TRY(cudaStreamWaitEvent(cs, hp.d2h[q], 0));  // chunk k-2's results are out of slot q
     tr.mark(cs, "solve " + std::to_string(k) + " start");
     if (b->perm_from_seed)
-      if (int rc = shuffle_seeded(cnt, reinterpret_cast<const int32_t*>(D + o_m),
+      if (int rc = shuffle_seeded(o->scheduler == LP2D_SCHED_BALANCED, cnt, reinterpret_cast<const int32_t*>(D + o_m),
                                   reinterpret_cast<const int64_t*>(D + o_off), kmax[k], b->perm_seed,
                                   b->perm_first + c0, b->perm_mul, b->perm_add, dperm,
                                   b->perm_bits, cs))
@@ -1257,6 +1310,10 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     if (int rc = solve_device_batch<S>(kp, E, e0, kmin[k], kmax[k], b->perm_bits, o->scheduler, dev,
                                        cs, true))
       return rc;
+    if (d.perm_wait_m != INT64_MAX) {  // (not consumed by a binned launch)
+      d.perm_wait_m = INT64_MAX;
+      CUDA_TRY(cudaStreamWaitEvent(cs, d.perm_ev, 0));
+    }
     CUDA_TRY(cudaEventRecord(hp.solved[q], cs));
     tr.mark(cs, "solve " + std::to_string(k) + " done");
     CUDA_TRY(cudaStreamWaitEvent(cb, hp.solved[q], 0));
@@ -1349,7 +1406,7 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
       kp.hist_stride = (int32_t)(b->max_m + 1);
     }
     if (b->perm_from_seed)
-      if (int rc = shuffle_seeded(b->n, b->m, b->offset, b->max_m, b->perm_seed, b->perm_first,
+      if (int rc = shuffle_seeded(false, b->n, b->m, b->offset, b->max_m, b->perm_seed, b->perm_first,
                                   b->perm_mul, b->perm_add, const_cast<void*>(b->perm), b->perm_bits,
                                   static_cast<cudaStream_t>(o->stream)))
         return rc;

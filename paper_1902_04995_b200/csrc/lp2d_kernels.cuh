@@ -1434,11 +1434,13 @@ __device__ __forceinline__ uint64_t derive_seed_dev(uint64_t base, uint64_t stre
 
 template <typename P>
 __global__ void k_shuffle_seeded(int64_t n, const int32_t* m, const int64_t* offset, uint64_t seed,
-                                 int64_t first, int32_t mul, int32_t add, P* perm, int32_t ps) {
+                                 int64_t first, int32_t mul, int32_t add, P* perm, int32_t ps,
+                                 int32_t big_lo, int32_t big_hi) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int32_t mj = m[j];
+  if (mj > big_lo && mj <= big_hi) return;  // k_shuffle_seeded_big's
   P* g = perm + offset[j];
   Xoshiro r(derive_seed_dev(seed, (uint64_t)((int64_t)mul * (first + j) + add)));
   const bool in_smem = mj <= ps;
@@ -1455,6 +1457,42 @@ __global__ void k_shuffle_seeded(int64_t n, const int32_t* m, const int64_t* off
     const uint4* src = reinterpret_cast<const uint4*>(o);
     uint4* dst = reinterpret_cast<uint4*>(g);
     for (int32_t v = 0; v < (mj + V - 1) / V; ++v) dst[v] = src[v];
+  }
+}
+
+// LPs with big_lo < m <= big_hi: one CTA per LP (grid-stride over the
+// batch), the whole permutation in shared memory. Fisher-Yates is one serial
+// chain: thread 0 runs it against shared memory (no L2 round trip per swap),
+// the other threads fill the identity and stream the result out. (Drawing
+// the generator's raw outputs in batches ahead of the swap loop measured
+// slower.)
+template <typename P>
+__global__ void __launch_bounds__(64) k_shuffle_seeded_big(int64_t n, const int32_t* m,
+                                                           const int64_t* offset, uint64_t seed,
+                                                           int64_t first, int32_t mul, int32_t add,
+                                                           P* perm, int32_t big_lo, int32_t big_hi) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  P* o = reinterpret_cast<P*>(smem);
+  for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
+    const int32_t mj = m[j];
+    if (mj <= big_lo || mj > big_hi) continue;
+    for (int32_t i = threadIdx.x; i < mj; i += blockDim.x) o[i] = (P)i;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Xoshiro r(derive_seed_dev(seed, (uint64_t)((int64_t)mul * (first + j) + add)));
+      for (int64_t i = mj; i > 1; --i) {
+        const uint64_t q = r.below((uint64_t)i);
+        const P tmp = o[i - 1];
+        o[i - 1] = o[q];
+        o[q] = tmp;
+      }
+    }
+    __syncthreads();
+    constexpr int V = 16 / (int)sizeof(P);
+    const uint4* src = reinterpret_cast<const uint4*>(o);
+    uint4* dst = reinterpret_cast<uint4*>(perm + offset[j]);
+    for (int32_t v = threadIdx.x; v < (mj + V - 1) / V; v += blockDim.x) dst[v] = src[v];
+    __syncthreads();
   }
 }
 

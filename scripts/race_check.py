@@ -27,7 +27,13 @@ for it in range(8):
     f8 = np.float64
     hout = P.PackedResult(*(pin(np.zeros(sh, d)) for sh, d in (
         (n, np.uint8), (n, f8), (n, f8), (n, f8), ((n, 2), np.int32), (n, np.uint32), (n, np.uint64))))
-    P.solve_packed(hps[i], P.BlockConfig(workers=1), out=hout)
+    if len(sys.argv) > 2 and sys.argv[2] == "seed":  # permutations generated on the device
+        hb = hps[i]
+        nop = P.PackedBatch(hb.m, hb.offset, hb.ax, hb.ay, hb.b, None, hb.c, hb.M)
+        P.solve_packed(nop, P.BlockConfig(workers=1), out=hout,
+                       perm_seed=P.PermSeed(bench.CONFIGS[cfg][3], 2, 1, i * pbs[0].n))
+    else:
+        P.solve_packed(hps[i], P.BlockConfig(workers=1), out=hout)
     st, x, y = exp[i]
     nb = int(np.sum((hout.status != st) | ~((hout.x == x) | (np.isnan(hout.x) & np.isnan(x)))))
     bad += nb
