@@ -957,6 +957,17 @@ std::vector<int64_t> plan_chunks(const int64_t* offset, int64_t lo, int64_t hi, 
     cut.push_back(j);
     start = j;
   }
+  // Taper: only the last chunk's solve is not hidden behind a transfer, so a
+  // large last chunk is cut at 3/4 of its elements.
+  const size_t k = cut.size();
+  if (k >= 2 && max_elems >= 4) {
+    const int64_t a = cut[k - 2], b = cut[k - 1];
+    const int64_t target = offset[a] + (offset[b] - offset[a]) * 3 / 4;
+    if (offset[b] - offset[a] > max_elems / 4) {
+      int64_t j = (int64_t)(std::upper_bound(offset + a + 1, offset + b + 1, target) - offset) - 1;
+      if (j > a && j < b) cut.insert(cut.end() - 1, j);
+    }
+  }
   return cut;
 }
 

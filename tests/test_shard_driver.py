@@ -43,11 +43,13 @@ def test_mock_shards_and_chunks(P, n_gpus, mock, chunk):
     for g in range(use):
         assert (shard[cut[g]:cut[g + 1]] == g).all()
     # chunks: contiguous runs inside a shard, each within the element budget
-    # (or a single LP), covering the shard
+    # (or a single LP), covering the shard; greedy except that the shard's
+    # last greedy chunk may be cut in two (the taper)
     off = np.asarray(d["offset"], np.int64)
     first = np.asarray(d["chunk"], np.int64)
     for g in range(use):
         lo, hi = cut[g], cut[g + 1]
+        runs = []
         j = lo
         while j < hi:
             c0 = first[j]
@@ -56,9 +58,12 @@ def test_mock_shards_and_chunks(P, n_gpus, mock, chunk):
             while k < hi and first[k] == c0:
                 k += 1
             assert k - j == 1 or off[k] - off[j] <= chunk
-            if k < hi:  # greedy: the next LP would have overflowed the chunk
-                assert off[k + 1] - off[j] > chunk
+            runs.append((j, k))
             j = k
+        for i, (j, k) in enumerate(runs[:-1]):
+            tapered = i == len(runs) - 2 and off[hi] - off[j] <= chunk
+            if not tapered:  # greedy: the next LP would have overflowed the chunk
+                assert off[k + 1] - off[j] > chunk
 
 
 def test_partition_balances_work(P):
