@@ -68,12 +68,9 @@ struct DeviceState {
   cudaStream_t cls_stream[16] = {};
   cudaEvent_t cls_event[17] = {};
   // Host mode with perm_from_seed: the large LPs' permutations are shuffled
-  // on aux while the rest of the chunk proceeds; only size classes that can
-  // hold an LP with m > perm_wait_m wait for perm_ev (set by shuffle_seeded,
-  // consumed by launch_binned; under mu, the host thread owns the device).
+  // on aux while the rest of the chunk proceeds (see PermWait).
   cudaStream_t aux = nullptr;
   cudaEvent_t perm_ev = nullptr;
-  int64_t perm_wait_m = INT64_MAX;
   // Stream-ordered workspace pool (binning lists) that keeps its memory:
   // the default pool returns freed memory at every synchronisation, making
   // the next allocation remap it (milliseconds, randomly).
@@ -81,6 +78,17 @@ struct DeviceState {
 };
 
 DeviceState g_dev[64];
+
+// The pending wait of a split shuffle (shuffle_seeded with split): only size
+// classes that can hold an LP with m > wait_m wait for the device's perm_ev.
+// Set and consumed by the same host thread (the shard's, holding the
+// device's mu), so a concurrent device-mode call on another thread never
+// sees it.
+struct PermWait {
+  int dev = -1;
+  int64_t wait_m = INT64_MAX;
+};
+thread_local PermWait t_perm_wait;
 
 // Restores the caller's current device (torch and others rely on it).
 struct DeviceGuard {
@@ -578,9 +586,9 @@ int launch_binned(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStream_
   const int cmin = class_of<T>(std::max<int64_t>(min_m, 0));
   const int cmax = class_of<T>(max_m);
   DeviceState& dv = g_dev[dev];
-  const int64_t perm_wait_m = dv.perm_wait_m;
-  dv.perm_wait_m = INT64_MAX;
-  const bool perm_wait = perm_wait_m != INT64_MAX;
+  const bool perm_wait = t_perm_wait.dev == dev && t_perm_wait.wait_m != INT64_MAX;
+  const int64_t perm_wait_m = t_perm_wait.wait_m;
+  t_perm_wait = PermWait{};
   if (cmin == cmax) {
     if (perm_wait) CUDA_TRY(cudaStreamWaitEvent(s, dv.perm_ev, 0));
     return launch_cls(kp, cmax, dev, s, max_m);
@@ -909,7 +917,7 @@ int shuffle_seeded(bool split, int64_t n, const int32_t* m, const int64_t* offse
     note_launch();
     if (split) {
       CUDA_TRY(cudaEventRecord(dv.perm_ev, dv.aux));
-      dv.perm_wait_m = big_lo;
+      t_perm_wait = PermWait{dev, big_lo};
     }
   }
   const int32_t skip_hi = (ps > 0 && big_hi > big_lo) ? big_hi : big_lo;
@@ -1321,8 +1329,8 @@ int solve_shard_host(int dev, const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_
     if (int rc = solve_device_batch<S>(kp, E, e0, kmin[k], kmax[k], b->perm_bits, o->scheduler, dev,
                                        cs, true))
       return rc;
-    if (d.perm_wait_m != INT64_MAX) {  // (not consumed by a binned launch)
-      d.perm_wait_m = INT64_MAX;
+    if (t_perm_wait.dev == dev) {  // (not consumed by a binned launch)
+      t_perm_wait = PermWait{};
       CUDA_TRY(cudaStreamWaitEvent(cs, d.perm_ev, 0));
     }
     CUDA_TRY(cudaEventRecord(hp.solved[q], cs));
