@@ -564,6 +564,71 @@ int launch_fx_class(const KParams& kp, int cls, int dev, cudaStream_t s, int64_t
   return fail(LP2D_ERR_UNSUPPORTED, "fx size class not built");
 }
 
+// ---- fp32 storage: K6 lane groups (k_solve_grp, lp2d_grp.cuh) -------------
+template <typename P, int G, int CAP>
+int launch_grp(KParams kp, int dev, cudaStream_t stream) {
+  using L = GrpLayout<P, G, CAP>;
+  auto kern = k_solve_grp<P, G, CAP>;
+  constexpr size_t smem = kGrpWarps * L::kWarpBytes;
+  static int blocks_per_sm[64] = {0};
+  static std::mutex mu;  // concurrent first use from multi-GPU host threads
+  int b = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!blocks_per_sm[dev]) {
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int q = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, kern, kGrpWarps * 32, smem));
+      if (q < 1) return fail(LP2D_ERR_CUDA, "group kernel does not fit on an SM");
+      blocks_per_sm[dev] = q;
+    }
+    b = blocks_per_sm[dev];
+  }
+  const int64_t per_warp = L::kGroups;
+  const int64_t warps = (kp.n_list + per_warp - 1) / per_warp;
+  const int64_t want = (warps + kGrpWarps - 1) / kGrpWarps;
+  const int64_t maxb = (int64_t)b * g_dev[dev].sm_count;
+  const int grid = (int)std::max<int64_t>(1, std::min(want, maxb));
+  kp.total_warps = grid * kGrpWarps;
+  kp.counter = take_counter(dev);
+  kern<<<grid, kGrpWarps * 32, smem, stream>>>(kp);
+  note_launch();
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// Largest register-slot count whose class runs K6 (0: none). Default: the
+// m <= 60 class only, four lanes per LP (B200, config 4: 0.737 -> 0.720 ms per
+// isolated solve; m = 40: 3.01 vs 3.26 ns/LP with K4). Above m = 60 the
+// double-arithmetic fold loses to K4's certified fp32 fold (m = 128: 7.56 vs
+// 4.64 ns/LP; 46 vs 16 instructions per unit): those classes
+// run K6 (8 lanes per LP) only on request, LP2D_B200_GRP=6 (A/B, parity
+// tests); LP2D_B200_GRP=0 turns K6 off; LP2D_B200_FS=all keeps K5 everywhere.
+int grp_max_slots() {
+  static const int v = [] {
+    const char* e = std::getenv("LP2D_B200_GRP");
+    if (!e) return 2;
+    return std::atoi(e);
+  }();
+  return v;
+}
+
+bool grp_class(int cls) {
+  return cls >= 1 && cls < n_reg_classes<double>() && kSlotClasses[cls] <= grp_max_slots() &&
+         kSlotClasses[cls] <= 6 && fs_mode() != 2;
+}
+
+template <typename P>
+int launch_grp_class(const KParams& kp, int cls, int dev, cudaStream_t s) {
+  switch (kSlotClasses[cls]) {
+    case 2: return launch_grp<P, 4, 60>(kp, dev, s);
+    case 4: return launch_grp<P, 8, 124>(kp, dev, s);
+    case 5: return launch_grp<P, 8, 156>(kp, dev, s);
+    case 6: return launch_grp<P, 8, 188>(kp, dev, s);
+  }
+  return fail(LP2D_ERR_UNSUPPORTED, "group size class not built");
+}
+
 template <typename T, typename F>
 int launch_binned(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStream_t s,
                   bool may_sync, F&& launch_cls);
@@ -829,6 +894,7 @@ int solve_f32_balanced(KParams kp, int64_t E, int64_t min_m, int64_t max_m, int 
         static const bool force_cta = std::getenv("LP2D_B200_FORCE_CTA") &&
                                       std::getenv("LP2D_B200_FORCE_CTA")[0] == '1';
         if (force_cta && c >= 1) return launch_cta_kernel<double, P, float>(kc, cap_m, d, cs);
+        if (grp_class(c)) return launch_grp_class<P>(kc, c, d, cs);
         if (fx_class(c)) return launch_fx_class<P>(kc, c, d, cs, cap_m);
         // the lane class (m <= 28) and the CTA class (large LPs) read the
         // float storage directly and widen on load (exact)

@@ -1575,3 +1575,4 @@ __global__ void k_generate(int64_t n, int64_t first, uint64_t seed, const int32_
 #include "lp2d_warp.cuh"
 #include "lp2d_fx.cuh"
 #include "lp2d_fs.cuh"
+#include "lp2d_grp.cuh"

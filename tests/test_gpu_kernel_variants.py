@@ -12,9 +12,13 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("mode", ["0", "all"])
-def test_fp32_kernel_variant_parity(mode):
-    env = dict(os.environ, LP2D_B200_FS=mode)
+@pytest.mark.parametrize("knobs", [{"LP2D_B200_FS": "0"}, {"LP2D_B200_FS": "all"},
+                                   {"LP2D_B200_GRP": "6"}, {"LP2D_B200_GRP": "0"}],
+                         ids=["k4", "k5-all", "k6-all", "k6-off"])
+def test_fp32_kernel_variant_parity(knobs):
+    """K4 (default above m = 60), K5 for every warp class, K6 lane groups for
+    every class up to m = 188 (default: m <= 60 only), and K6 off."""
+    env = dict(os.environ, **knobs)
     r = subprocess.run([sys.executable, os.path.join(HERE, "variant_check.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]

@@ -1,5 +1,5 @@
 """Parity of one fp32-storage kernel variant, run in a fresh process because
-the library reads its kernel-selection knob (LP2D_B200_FS) once:
+the library reads its kernel-selection knobs (LP2D_B200_FS, LP2D_B200_GRP) once:
     LP2D_B200_FS=all python tests/variant_check.py
 Every fp32 fixture against the UNMODIFIED reference's results on the rounded
 instance, the size-class edges and a heavy-tailed batch against the oracle."""
@@ -45,7 +45,8 @@ def main():
     for m, n, seed in ((128, 4096, 3), (500, 2048, 7), (1024, 1024, 2)):
         pb = P.PackedBatch.generate(np.full(n, m, np.int32), seed).astype(np.float32)
         same(P.solve_packed(pb), O.solve_batch(pb, threads=16), f"m={m}")
-    print("variant %s ok" % os.environ.get("LP2D_B200_FS", "default"))
+    print("variant FS=%s GRP=%s ok" % (os.environ.get("LP2D_B200_FS", "default"),
+                                        os.environ.get("LP2D_B200_GRP", "default")))
 
 
 if __name__ == "__main__":
