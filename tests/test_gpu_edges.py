@@ -52,7 +52,7 @@ def _same(r, o, O, what):
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
 def test_adversarial_ordered_every_step_violates(P, O, dt):
-    sizes = [16, 64, 100, 300, 700, 1000, 2048]
+    sizes = [16, 40, 60, 64, 100, 300, 700, 1000, 2048]
     rp = _adversarial_batch(O, sizes, 3, shuffled=False)
     pb = _packed(P, rp, dt)
     o = O.solve_batch(pb)

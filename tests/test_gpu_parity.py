@@ -397,3 +397,27 @@ def test_device_generator_streams_and_parity(P, O):
         feas = o["status"] != O.INFEASIBLE
         assert np.array_equal(out.x.cpu().numpy()[feas].astype(np.float64), o["x"][feas])
         assert np.array_equal(out.work_units.cpu().numpy().astype(np.uint64), o["work_units"])
+
+
+def test_small_lps_lane_groups(P, O):
+    """29 <= m <= 60 in fp32 storage runs K6 (4 lanes per LP, 8 LPs per warp,
+    k_solve_grp): all generator kinds, every size of the class, wild
+    magnitudes (exact refold per group), an invalid permutation (status 255
+    for that LP only), uniform and binned launches."""
+    rng = np.random.default_rng(12)
+    m = rng.integers(29, 61, 2000).astype(np.int32)
+    kind = rng.choice([P.GenKind.feasible_random, P.GenKind.infeasible,
+                       P.GenKind.unbounded_random], 2000).astype(np.uint8)
+    pb = P.PackedBatch.generate(m, 41, kind=kind).astype(np.float32)
+    pb.ax[:int(pb.offset[50])] *= np.float32(1e20)
+    pb.b[int(pb.offset[100]):int(pb.offset[150])] *= np.float32(1e-30)
+    pb.ay[int(pb.offset[200]):int(pb.offset[230])] = 0.0
+    assert_same_as_oracle(P.solve_packed(pb), O.solve_batch(pb), O, "k6")
+    bad = pb.subset(0, 64)
+    bad.perm = bad.perm.copy()
+    bad.perm[int(bad.offset[5]) + 7] = 1000
+    rb = P.solve_packed(bad)
+    assert rb.status[5] == 255 and (np.delete(rb.status, 5) != 255).all()
+    mix = P.PackedBatch.generate(np.concatenate([m[:800], rng.integers(1, 400, 400)]).astype(np.int32),
+                                 42).astype(np.float32)
+    assert_same_as_oracle(P.solve_packed(mix), O.solve_batch(mix), O, "k6+mixed")
