@@ -1495,9 +1495,16 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
                                   b->perm_mul, b->perm_add, const_cast<void*>(b->perm), b->perm_bits,
                                   static_cast<cudaStream_t>(o->stream)))
         return rc;
-    int64_t E = 0;  // scalar elements (offset[n]), needed to widen fp32 storage
+    // scalar elements (offset[n]): only the naive scheduler on fp32 storage
+    // widens the batch and needs it; the balanced path stays asynchronous
+    // (no host round trip per call)
+    int64_t E = 0;
     if constexpr (sizeof(S) == 4) {
-      CUDA_TRY(cudaMemcpy(&E, b->offset + b->n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+      if (o->scheduler != LP2D_SCHED_BALANCED) {
+        const cudaStream_t st = static_cast<cudaStream_t>(o->stream);
+        CUDA_TRY(cudaMemcpyAsync(&E, b->offset + b->n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+      }
     }
     return solve_device_batch<S>(kp, E, 0, b->min_m, b->max_m, b->perm_bits, o->scheduler, dev,
                                  static_cast<cudaStream_t>(o->stream), false);
