@@ -618,10 +618,16 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
     const FxLP C = fx_lp_consts(p, A, B, h.cx, h.cy);
     FxFrame F = fx_frame(C, 0.0f, 0.0f);
     bool shifted = false;  // frame != 0 (late-TMA classes: the buffer holds b')
+#ifdef LP2D_FX_LPSTATS
+    uint32_t st_res = 0, st_exe = 0, st_tst = 0;  // debug: per-LP path counts
+#endif
     // Move the frame to s = (nsx, nsy): b' of every constraint (register
     // chunks, and in place in the staging buffer for the late-TMA classes).
     auto reshift = [&](float nsx, float nsy) {
       fx_count(p, kFxReshift, lane);
+#ifdef LP2D_FX_LPSTATS
+      ++st_res;
+#endif
       if constexpr (L::kLateTma) {
         // b' of every staged constraint rewritten in place (original
         // order): from the staged original b on the first reshift, else
@@ -768,6 +774,9 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
         if (he < Sk - tol) continue;  // satisfied: resume the sweep after pi
         if (!(he > Sk + tol)) {
           fx_count(p, kFxTestFlag, lane);
+#ifdef LP2D_FX_LPSTATS
+          ++st_tst;
+#endif
           if (stale) fx_count(p, kFxLazy, lane);
           const bool v = fx_exact_violates<P>(p, h.off, h.M, pi, pos0, pos1, stale, xp, yp);
           stale = false;
@@ -896,6 +905,9 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
       if (!done) {
         // the reference's double operations for this event
         fx_count(p, kFxExact, lane);
+#ifdef LP2D_FX_LPSTATS
+        ++st_exe;
+#endif
         const int r = fx_exact_event<P>(p, h.lp, h.off, mj, pi, h.cx, h.cy, h.M, pos0, pos1, xp, yp,
                                         L::kLateTma ? sperm : nullptr, L::kLateTma ? sax : nullptr,
                                         L::kLateTma ? say : nullptr);
@@ -1012,6 +1024,9 @@ __global__ void __launch_bounds__(WarpLayout<float, P, NS, NT, CAP>::kMaxWarpsRt
       static_cast<double*>(p.value)[lp] = feas ? (double)h.cx * xp + (double)h.cy * yp : 0.0;
       if (p.viol) p.viol[lp] = viol;
       if (p.wu) p.wu[lp] = wu32;
+#ifdef LP2D_FX_LPSTATS  // debug: pair[2lp+1] = reshifts | exact events << 10 | exact tests << 20
+      if (p.pair) p.pair[2 * lp + 1] = (int32_t)(st_res | (st_exe << 10) | (st_tst << 20));
+#endif
 #ifdef LP2D_FX_TIMELINE
       uint64_t tl1;  // debug: wu = start (ns), pair[2lp] = duration (ns)
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl1));
