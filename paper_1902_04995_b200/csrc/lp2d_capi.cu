@@ -597,17 +597,19 @@ int launch_grp(KParams kp, int dev, cudaStream_t stream) {
   return 0;
 }
 
-// Largest register-slot count whose class runs K6 (0: none). Default: the
-// m <= 60 class only, four lanes per LP (B200, config 4: 0.737 -> 0.720 ms per
-// isolated solve; m = 40: 3.01 vs 3.26 ns/LP with K4). Above m = 60 the
-// double-arithmetic fold loses to K4's certified fp32 fold (m = 128: 7.56 vs
-// 4.64 ns/LP; 46 vs 16 instructions per unit): those classes
-// run K6 (8 lanes per LP) only on request, LP2D_B200_GRP=6 (A/B, parity
-// tests); LP2D_B200_GRP=0 turns K6 off; LP2D_B200_FS=all keeps K5 everywhere.
+// Largest register-slot count whose class runs K6 (0: none, the default).
+// K6 is an opt-in variant: it beats K4 only on large batches of m <= ~45
+// (m = 40: 3.01 vs 3.26 ns/LP over 2^17 LPs) and loses on config 4's own
+// m <= 60 LPs solved alone (38,863 LPs: 191 vs 143 us: ~2 LPs per group, and
+// its per-LP latency is 4-8 lanes' worth), at m = 60 (4.15 vs 3.51 ns/LP) and
+// above (the double fold: m = 128 7.56 vs 4.64 ns/LP); inside the
+// whole config-4 solve it is a wash under the final launch order (0.672/0.700
+// vs 0.682/0.680 ms). LP2D_B200_GRP=2 runs it on the m <= 60 class, =6 on
+// every class up to m = 188 (A/B, parity tests); LP2D_B200_FS=all keeps K5.
 int grp_max_slots() {
   static const int v = [] {
     const char* e = std::getenv("LP2D_B200_GRP");
-    if (!e) return 2;
+    if (!e) return 0;
     return std::atoi(e);
   }();
   return v;
@@ -715,7 +717,6 @@ int launch_binned(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStream_
   int rc = 0;
   // One stream per class, forked from and joined back into s: a class's
   // tail (few long LPs) overlaps the next classes instead of idling the GPU.
-  // Largest class first: its LPs are the longest, so they start earliest.
   {
     DeviceState& d = g_dev[dev];
     std::lock_guard<std::mutex> lock(d.fork_mu);
@@ -740,7 +741,28 @@ int launch_binned(KParams kp, int64_t min_m, int64_t max_m, int dev, cudaStream_
       CUDA_TRY(cudaStreamWaitEvent(s, d.cls_event[sidx], 0));
       return r;
     };
-    for (int c = cmax; c >= cmin && rc == 0; --c) {
+    // Launch order: the large (CTA) class first (its LPs are the longest and
+    // latency-bound, so they start earliest), then the register classes from
+    // the smallest up (B200, config 4 isolated solve: 0.708/0.712 ms largest
+    // first, 0.674/0.696 this order; 0.682/0.685 with the tiny classes next and
+    // the warp classes largest first; 0.697/0.698 smallest first throughout).
+    // LP2D_B200_ORDER = 0 / 2 / 3 selects those alternatives (A/B).
+    static const int order = std::getenv("LP2D_B200_ORDER") ? std::atoi(std::getenv("LP2D_B200_ORDER")) : 1;
+    std::vector<int> seq;
+    if (order == 1 && cmax == spec.nreg) {
+      seq.push_back(cmax);
+      for (int c = cmin; c < cmax; ++c) seq.push_back(c);
+    } else if (order == 2 && cmax == spec.nreg) {
+      seq.push_back(cmax);
+      for (int c = cmin; c < std::min(cmax, 2); ++c) seq.push_back(c);
+      for (int c = cmax - 1; c >= std::max(cmin, 2); --c) seq.push_back(c);
+    } else if (order == 3) {
+      for (int c = cmin; c <= cmax; ++c) seq.push_back(c);
+    } else {
+      for (int c = cmax; c >= cmin; --c) seq.push_back(c);
+    }
+    for (size_t si = 0; si < seq.size() && rc == 0; ++si) {
+      const int c = seq[si];
       if (may_sync && host_counts[c] == 0) continue;
       int lo, hi;
       bin_range(c, lo, hi);

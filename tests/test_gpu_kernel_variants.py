@@ -13,11 +13,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 @pytest.mark.parametrize("knobs", [{"LP2D_B200_FS": "0"}, {"LP2D_B200_FS": "all"},
-                                   {"LP2D_B200_GRP": "6"}, {"LP2D_B200_GRP": "0"}],
-                         ids=["k4", "k5-all", "k6-all", "k6-off"])
+                                   {"LP2D_B200_GRP": "6"}, {"LP2D_B200_GRP": "2"},
+                                   {"LP2D_B200_ORDER": "0"}],
+                         ids=["k4", "k5-all", "k6-all", "k6-small", "order-largest-first"])
 def test_fp32_kernel_variant_parity(knobs):
-    """K4 (default above m = 60), K5 for every warp class, K6 lane groups for
-    every class up to m = 188 (default: m <= 60 only), and K6 off."""
+    """K4 (the default warp classes), K5 for every warp class, K6 lane groups
+    for every class up to m = 188 or for m <= 60 only, and the mixed-batch
+    class launches in the largest-first order."""
     env = dict(os.environ, **knobs)
     r = subprocess.run([sys.executable, os.path.join(HERE, "variant_check.py")], env=env,
                        capture_output=True, text=True, timeout=600)

@@ -399,11 +399,11 @@ def test_device_generator_streams_and_parity(P, O):
         assert np.array_equal(out.work_units.cpu().numpy().astype(np.uint64), o["work_units"])
 
 
-def test_small_lps_lane_groups(P, O):
-    """29 <= m <= 60 in fp32 storage runs K6 (4 lanes per LP, 8 LPs per warp,
-    k_solve_grp): all generator kinds, every size of the class, wild
-    magnitudes (exact refold per group), an invalid permutation (status 255
-    for that LP only), uniform and binned launches."""
+def test_small_lps_class(P, O):
+    """29 <= m <= 60 in fp32 storage (K4 by default; K6 lane groups with
+    LP2D_B200_GRP=2, test_k6_lane_groups_small_class): all generator kinds,
+    every size of the class, wild magnitudes (exact refolds), an invalid
+    permutation (status 255 for that LP only), uniform and binned launches."""
     rng = np.random.default_rng(12)
     m = rng.integers(29, 61, 2000).astype(np.int32)
     kind = rng.choice([P.GenKind.feasible_random, P.GenKind.infeasible,
@@ -421,3 +421,18 @@ def test_small_lps_lane_groups(P, O):
     mix = P.PackedBatch.generate(np.concatenate([m[:800], rng.integers(1, 400, 400)]).astype(np.int32),
                                  42).astype(np.float32)
     assert_same_as_oracle(P.solve_packed(mix), O.solve_batch(mix), O, "k6+mixed")
+
+
+def test_k6_lane_groups_small_class():
+    """The same class through K6 (4 lanes per LP, 8 LPs per warp), in a fresh
+    process because the library reads LP2D_B200_GRP once."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, LP2D_B200_GRP="2")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(here, "test_gpu_parity.py") + "::test_small_lps_class"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
