@@ -14,7 +14,6 @@ cap c3 k_solve_fx --config c3
 cap c5 k_solve_warp --config c5
 cap c2f64 k_solve_warp --config c2 --dtype f64
 cap c4lanes k_solve_lanes --config c4
-cap c4grp k_solve_grp --config c4
 bash scripts/ncu_launches.sh c4 > gpurun_out/c4_kernels.txt 2>&1
 for r in gpurun_out/full_*.ncu-rep; do
   t=$(basename $r .ncu-rep); t=${t#full_}
