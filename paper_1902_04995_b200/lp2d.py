@@ -354,9 +354,15 @@ def _raise(rc: int):
     raise RuntimeError(f"lp2d_b200 error {rc}: {msg}")
 
 
+_OPTS0 = None
+
+
 def _opts(cfg: BlockConfig, tol: Tolerance, device: int = 0, stream: int = 0) -> N.Opts:
-    o = N.Opts()
-    N.lib().lp2dgpu_default_opts(C.byref(o))
+    global _OPTS0
+    if _OPTS0 is None:
+        _OPTS0 = N.Opts()
+        N.lib().lp2dgpu_default_opts(C.byref(_OPTS0))
+    o = N.Opts.from_buffer_copy(_OPTS0)
     o.scheduler = int(cfg.scheduler)
     o.block_width = int(cfg.block_width) if cfg.block_width < 2**31 else 2**31 - 1
     o.n_gpus = int(cfg.workers)
@@ -377,6 +383,19 @@ class PermSeed:
     mul: int = 2
     add: int = 1
     first: int = 0
+
+
+def _pointers(obj, arrays) -> tuple:
+    """Data pointers of `arrays`, cached on `obj` while it holds the very same
+    array objects (the cache keeps them alive, so identity is a safe key):
+    a repeated call with the same host batch / result buffers skips the
+    numpy->ctypes conversions (~3 us per array, ~40 us per call otherwise)."""
+    c = obj.__dict__.get("_ptr_cache")
+    if c is not None and len(c[0]) == len(arrays) and all(x is y for x, y in zip(c[0], arrays)):
+        return c[1]
+    ptrs = tuple(a.ctypes.data if a is not None else None for a in arrays)
+    obj.__dict__["_ptr_cache"] = (tuple(arrays), ptrs)
+    return ptrs
 
 
 def solve_packed(pb: PackedBatch, cfg: BlockConfig = BlockConfig(), tol: Tolerance = Tolerance(),
@@ -404,18 +423,17 @@ def solve_packed(pb: PackedBatch, cfg: BlockConfig = BlockConfig(), tol: Toleran
     pbits = 16 if perm.dtype == np.uint16 else 32
     if perm_seed is not None:
         pbits = 16 if int(pb.m.max(initial=0)) <= 65536 else 32
-    s = N.BatchSoA(pb.n, m.ctypes.data, off.ctypes.data, ax.ctypes.data, ay.ctypes.data,
-                   b.ctypes.data, perm.ctypes.data if perm_seed is None else None, pbits,
-                   N.MEM_HOST, c.ctypes.data, M.ctypes.data, 0, 0)
+    pm, po, pax, pay, pbb, pp, pc, pM = _pointers(pb, arrs)
+    s = N.BatchSoA(len(m), pm, po, pax, pay, pbb, pp if perm_seed is None else None, pbits,
+                   N.MEM_HOST, pc, pM, 0, 0)
     if perm_seed is not None:
         s.perm_from_seed = 1
         s.perm_mul, s.perm_add = int(perm_seed.mul), int(perm_seed.add)
         s.perm_seed = perm_seed.seed & (2**64 - 1)
         s.perm_first = int(perm_seed.first)
     o = _opts(cfg, tol)
-    r = N.Out(out.status.ctypes.data, out.x.ctypes.data, out.y.ctypes.data, out.value.ctypes.data,
-              out.pair.ctypes.data, out.violation_events.ctypes.data, out.work_units.ctypes.data,
-              iter_hist.ctypes.data if iter_hist is not None else None)
+    r = N.Out(*_pointers(out, (out.status, out.x, out.y, out.value, out.pair, out.violation_events,
+                               out.work_units, iter_hist)))
     fn = N.lib().lp2dgpu_solve_f32 if dt == np.float32 else N.lib().lp2dgpu_solve_f64
     rc = fn(C.byref(s), C.byref(o), C.byref(r))
     if rc:
