@@ -684,6 +684,9 @@ __global__ void __launch_bounds__(128) k_solve_naive(const __grid_constant__ KPa
 // warp kernel. Box positions 0..3 are constants, not stored.
 constexpr int kLaneWarps = 4;
 constexpr int kLaneMaxM = 28;
+#ifndef LP2D_LANE_MINB
+#define LP2D_LANE_MINB 4  // resident CTAs per SM the lane kernel's registers allow
+#endif
 
 template <typename T, int MAXM>
 struct LaneTile {
@@ -712,7 +715,7 @@ __device__ __forceinline__ Line<T> shfl_line(const Line<T>& l, int src) {
 // S: storage type of the batch's scalars (float storage is widened exactly on
 // load; the arithmetic is T's, the fp32 configs' double semantics).
 template <typename T, typename P, int MAXM, typename S = T>
-__global__ void __launch_bounds__(kLaneWarps * 32, 4) k_solve_lanes(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kLaneWarps * 32, LP2D_LANE_MINB) k_solve_lanes(const __grid_constant__ KParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   // the tile holds the STORED scalars (float storage: half the shared memory
   // of a double tile, so twice the resident warps); reads widen exactly
