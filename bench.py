@@ -621,8 +621,11 @@ def hold_gpu(torch, stream, ms=20.0):
     enqueues the K steps while the GPU is still busy: the CUDA events then see
     only device work, never a GPU idling on the host's launch path (which
     would dominate steps of a few tens of microseconds, e.g. config 1)."""
+    sleep = getattr(torch.cuda, "_sleep", None)
+    if sleep is None:  # (private torch API; without it the region just starts idle)
+        return
     with torch.cuda.stream(stream):
-        torch.cuda._sleep(int(ms * 1e-3 * 1.9e9))
+        sleep(int(ms * 1e-3 * 1.9e9))
 
 
 def _pinned_copy(torch, a):
