@@ -531,14 +531,14 @@ def main():
     hout = P.PackedResult(*(pin(np.zeros(sh, d)) for sh, d in (
         (n, np.uint8), (n, f8), (n, f8), (n, f8), ((n, 2), np.int32), (n, np.uint32), (n, np.uint64))))
     cfgb = P.BlockConfig(workers=1)
-    P.solve_packed(hp, cfgb, out=hout)  # warm the library's device arena
+    P.solve_packed(hp, cfgb, out=hout, device=local)  # warm the library's device arena
     h2d = sum(a.nbytes for a in (hp.m, hp.offset, hp.ax, hp.ay, hp.b, hp.perm, hp.c, hp.M))
     d2h = sum(a.nbytes for a in (hout.status, hout.x, hout.y, hout.value, hout.pair,
                                  hout.violation_events, hout.work_units))
     barrier()
     te0 = time.perf_counter()
     for _ in range(e2e_steps):
-        P.solve_packed(hp, cfgb, out=hout)
+        P.solve_packed(hp, cfgb, out=hout, device=local)
     te1 = time.perf_counter()
     barrier()
     e2e_s = max_over_ranks(te1 - te0)
@@ -549,11 +549,11 @@ def main():
     first = rank * n
     hp_np = P.PackedBatch(hp.m, hp.offset, hp.ax, hp.ay, hp.b, None, hp.c, hp.M)
     ps = P.PermSeed(seed, 2, 1, first)
-    P.solve_packed(hp_np, cfgb, out=hout, perm_seed=ps)
+    P.solve_packed(hp_np, cfgb, out=hout, perm_seed=ps, device=local)
     barrier()
     te0 = time.perf_counter()
     for _ in range(e2e_steps):
-        P.solve_packed(hp_np, cfgb, out=hout, perm_seed=ps)
+        P.solve_packed(hp_np, cfgb, out=hout, perm_seed=ps, device=local)
     te1 = time.perf_counter()
     barrier()
     e2e_ps_value = world * pb.n * e2e_steps / max_over_ranks(te1 - te0)

@@ -117,7 +117,9 @@ typedef struct lp2d_opts {
                           schedule is fixed by the kernel, see DESIGN.md */
   int32_t n_gpus;      /* host mode: shard over this many visible devices
                           (0 = all); replaces block_config::workers */
-  int32_t device;      /* device mode: device ordinal of the pointers */
+  int32_t device;      /* device mode: device ordinal of the pointers; host
+                          mode with n_gpus == 1: the device that solves (e.g.
+                          a rank's local GPU; out of range = device 0) */
   void* stream;        /* device mode: cudaStream_t (NULL = legacy stream) */
   double eps_parallel; /* core.hpp:60 (1e-12) */
   double eps_feas;     /* core.hpp:61 (1e-9)  */

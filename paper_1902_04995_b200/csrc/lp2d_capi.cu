@@ -1555,14 +1555,17 @@ int solve_impl(const lp2d_batch_soa* b, const lp2d_opts* o, lp2d_out* out) {
   // (overlapped with the previous chunk's transfer); otherwise up front.
   int use = o->n_gpus > 0 ? std::min(o->n_gpus, ndev) : ndev;
   use = (int)std::min<int64_t>(std::min(use, 64), b->n);
-  if (use == 1 && !out->iter_hist) return solve_shard_host<S>(0, b, o, out, 0, b->n, -1, -1);
+  // a single-device call solves on opts.device (one process per GPU, e.g.
+  // a torchrun rank's local GPU); shards of a multi-device call on 0..use-1
+  const int dev1 = (use == 1 && !mock && o->device >= 0 && o->device < std::min(ndev, 64)) ? o->device : 0;
+  if (use == 1 && !out->iter_hist) return solve_shard_host<S>(dev1, b, o, out, 0, b->n, -1, -1);
   int64_t min_m = 0, max_m = 0;
   if (int rc = scan_layout(b, 0, b->n, min_m, max_m)) return rc;
   trace_host("validated", th0);
   if (out->iter_hist)
     std::memset(out->iter_hist, 0,
                 sizeof(uint32_t) * ((b->n + o->block_width - 1) / o->block_width) * (max_m + 1));
-  if (use == 1) return solve_shard_host<S>(0, b, o, out, 0, b->n, min_m, max_m);
+  if (use == 1) return solve_shard_host<S>(dev1, b, o, out, 0, b->n, min_m, max_m);
   std::vector<int64_t> cut(use + 1, 0);
   lp2dgpu_partition(b->n, b->m, use, cut.data());
   std::vector<int> rcs(use, 0);

@@ -401,10 +401,11 @@ def _pointers(obj, arrays) -> tuple:
 def solve_packed(pb: PackedBatch, cfg: BlockConfig = BlockConfig(), tol: Tolerance = Tolerance(),
                  out: Optional[PackedResult] = None,
                  iter_hist: Optional[np.ndarray] = None,
-                 perm_seed: Optional[PermSeed] = None) -> PackedResult:
+                 perm_seed: Optional[PermSeed] = None, device: int = 0) -> PackedResult:
     """Host-buffer solve through the C ABI (copies in/out inside the call).
     With perm_seed, pb.perm is ignored (may be None): the permutations are
-    generated on the device and never cross PCIe."""
+    generated on the device and never cross PCIe. device: the GPU of a
+    single-device call (cfg.workers == 1), e.g. a rank's local GPU."""
     if pb.n == 0:
         raise ValueError("solve_batch: empty batch")
     dt = pb.dtype
@@ -431,7 +432,7 @@ def solve_packed(pb: PackedBatch, cfg: BlockConfig = BlockConfig(), tol: Toleran
         s.perm_mul, s.perm_add = int(perm_seed.mul), int(perm_seed.add)
         s.perm_seed = perm_seed.seed & (2**64 - 1)
         s.perm_first = int(perm_seed.first)
-    o = _opts(cfg, tol)
+    o = _opts(cfg, tol, device=device)
     r = N.Out(*_pointers(out, (out.status, out.x, out.y, out.value, out.pair, out.violation_events,
                                out.work_units, iter_hist)))
     fn = N.lib().lp2dgpu_solve_f32 if dt == np.float32 else N.lib().lp2dgpu_solve_f64
